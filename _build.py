@@ -1,0 +1,84 @@
+"""In-tree build of the three native libraries (no JIT cache; the .so files travel with
+the repo snapshot to the GPU box).
+
+  synth/libsynth.so                      seeded input generators (gcc)
+  oracle/liboracle.so                    scalar CPU oracle (gcc; test infrastructure only)
+  paper_1903_10107_b200/libqkdldpc.so    the product: sm_100a kernels + C ABI (nvcc)
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("build failed: " + " ".join(cmd))
+
+
+def build_synth(force: bool = False) -> str:
+    src = os.path.join(ROOT, "synth", "synth.c")
+    out = os.path.join(ROOT, "synth", "libsynth.so")
+    if force or _stale(out, [src]):
+        _run(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-o", out, src])
+    return out
+
+
+def build_oracle(force: bool = False) -> str:
+    src = os.path.join(ROOT, "oracle", "oracle.c")
+    out = os.path.join(ROOT, "oracle", "liboracle.so")
+    if force or _stale(out, [src]):
+        # -O2, scalar, no intrinsics, no -ffast-math (SURVEY §8(d) oracle build)
+        _run(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-o", out, src, "-lm"])
+    return out
+
+
+def cuda_sources() -> list[str]:
+    d = os.path.join(ROOT, "paper_1903_10107_b200", "csrc")
+    srcs = [os.path.join(d, f) for f in sorted(os.listdir(d)) if f.endswith((".cu", ".cuh", ".h"))]
+    srcs.append(os.path.join(ROOT, "include", "qkd_ldpc.h"))
+    return srcs
+
+
+def build_cuda(force: bool = False, extra: list[str] | None = None) -> str:
+    srcs = cuda_sources()
+    out = os.path.join(ROOT, "paper_1903_10107_b200", "libqkdldpc.so")
+    if force or extra or _stale(out, srcs + [__file__]):
+        cu = [s for s in srcs if s.endswith(".cu")]
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+               "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-o", out, *cu]
+        if extra:
+            cmd[1:1] = extra
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)
+        log = os.path.join(ROOT, "paper_1903_10107_b200", "ptxas.log")
+        with open(log, "w") as f:
+            f.write(r.stdout + r.stderr)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc build failed")
+    return out
+
+
+def build_all(force: bool = False) -> None:
+    build_synth(force)
+    build_oracle(force)
+    build_cuda(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)
+    print("built")
