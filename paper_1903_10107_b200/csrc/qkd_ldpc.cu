@@ -1,0 +1,740 @@
+// qkd_ldpc.cu -- B200 (sm_100a) batched quantized LDPC syndrome decoder + C ABI.
+// See include/qkd_ldpc.h for the contract and DESIGN.md for the design.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "decode.cuh"
+#include "qkd_ldpc.h"
+
+using namespace qkd;
+
+// --------------------------------------------------------------------------------------
+// errors
+// --------------------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+}  // namespace
+#define QKD_CK(x)                                                                    \
+    do {                                                                             \
+        cudaError_t e_ = (x);                                                        \
+        if (e_ != cudaSuccess)                                                       \
+            return fail(QKD_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// --------------------------------------------------------------------------------------
+// code handle
+// --------------------------------------------------------------------------------------
+struct qkd_code {
+    int32_t Mb = 0, Nb = 0, Z = 0;
+    int64_t n = 0, m = 0, n_edges = 0;
+    int32_t nbase = 0, maxdeg = 0;
+    std::vector<int2> layer;   // (deg, first base edge)
+    std::vector<int2> edge;    // (J*Z, shift)
+    int2* d_layer = nullptr;
+    int2* d_edge = nullptr;
+    uint8_t* d_kind = nullptr;     // pos kind or null
+    uint8_t* d_payload = nullptr;  // packed payload mask or null (= all payload)
+    bool has_short = false;
+    int device = 0;
+};
+
+// --------------------------------------------------------------------------------------
+// decode kernel: persistent CTAs; each "slot" (TG threads, own named barrier) decodes
+// frame groups of 4 frames taken from an atomic work counter.
+// --------------------------------------------------------------------------------------
+namespace {
+
+constexpr int kFramesPerGroup = 4;
+
+template <int DMAX, bool ESM>
+__device__ __forceinline__ void layer_pass(const DecParams& p, int d, const int2* et, int t, uint32_t* E,
+                                           uint32_t* Lrow, const uint8_t* synI, bool first) {
+    if constexpr (DMAX > 0) {
+        switch (d) {
+#define QKD_CASE(DD)                                                                      \
+    case DD:                                                                              \
+        if constexpr (DD <= DMAX) {                                                       \
+            for (int r = t; r < p.Z; r += p.TG) row_update<DD, ESM>(et, p.Z, r, E, Lrow, synI[r], first); \
+            return;                                                                       \
+        }                                                                                 \
+        break;
+            QKD_CASE(1) QKD_CASE(2) QKD_CASE(3) QKD_CASE(4) QKD_CASE(5) QKD_CASE(6) QKD_CASE(7)
+            QKD_CASE(8) QKD_CASE(9) QKD_CASE(10) QKD_CASE(11) QKD_CASE(12) QKD_CASE(13)
+            QKD_CASE(14) QKD_CASE(15) QKD_CASE(16) QKD_CASE(17) QKD_CASE(18) QKD_CASE(19)
+            QKD_CASE(20)
+#undef QKD_CASE
+            default:
+                break;
+        }
+        __trap();   // the host never selects a DMAX kernel for a code with a larger degree
+    } else {
+        for (int r = t; r < p.Z; r += p.TG) row_update_generic<ESM>(et, d, p.Z, r, E, Lrow, synI[r], first);
+    }
+}
+
+// per-lane syndrome violation mask (bit f set = frame f violates some parity check),
+// group-uniform.  Hard decision bit = (E < 0) = NOT bit 7 of E' (R9).
+template <bool ESM>
+__device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int2* s_layer, const int2* s_edge,
+                                                  const uint32_t* E, const uint8_t* sSyn, int t,
+                                                  uint32_t* flags, int& chk, int bar) {
+    uint32_t v = 0;
+    for (int I = 0; I < p.Mb; ++I) {
+        const int2 li = s_layer[I];
+        const int2* et = s_edge + li.y;
+        const uint32_t par = (li.x & 1) ? 0x80808080u : 0u;
+        for (int r = t; r < p.Z; r += p.TG) {
+            uint32_t acc = nib_to_bit7(sSyn[I * p.Z + r]) ^ par;
+            for (int k = 0; k < li.x; ++k) {
+                const int2 e = et[k];
+                int idx = r + e.y;
+                idx = idx >= p.Z ? idx - p.Z : idx;
+                acc ^= ldE<ESM>(E, e.x + idx);
+            }
+            v |= acc;
+        }
+    }
+    v &= 0x80808080u;
+    v = __reduce_or_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && v) atomicOr(&flags[chk & 1], v);
+    group_bar(bar, p.TG);
+    const uint32_t res = *(volatile uint32_t*)&flags[chk & 1];
+    if (t == 0) flags[(chk + 1) & 1] = 0;   // next check's flag: last read before this barrier
+    ++chk;
+    return ((res >> 7) & 1u) | ((res >> 14) & 2u) | ((res >> 21) & 4u) | ((res >> 28) & 8u);
+}
+
+// write the outputs of the lanes in `mask` (state at their stopping iteration)
+template <bool ESM>
+__device__ void finalize(const DecParams& p, const uint32_t* E, const uint32_t* Lg, long long f0, uint32_t mask,
+                         int it, uint32_t succ_mask, bool first, int t) {
+    const int lane = threadIdx.x & 31;
+    for (int f = 0; f < kFramesPerGroup; ++f) {
+        if (!((mask >> f) & 1u)) continue;
+        const long long frame = f0 + f;
+        uint8_t* brow = p.bits + frame * p.nb8;
+        for (int jw = t & ~31; jw < p.n; jw += p.TG) {
+            const int j = jw + lane;
+            const bool b = j < p.n && !((ldE<ESM>(E, j < p.n ? j : 0) >> (8 * f + 7)) & 1u);
+            const uint32_t bal = __ballot_sync(0xffffffffu, b);
+            const int byte = (jw >> 3) + lane;
+            if (lane < 4 && byte < p.nb8) brow[byte] = (uint8_t)(bal >> (8 * lane));
+        }
+        if (p.fE) {
+            int8_t* erow = p.fE + frame * p.n;
+            for (int j = t; j < p.n; j += p.TG) erow[j] = (int8_t)(((ldE<ESM>(E, j) >> (8 * f)) & 0xFFu) ^ 0x80u);
+        }
+        if (p.fL) {
+            int8_t* lrow = p.fL + frame * p.n_edges;
+            for (long long e = t; e < p.n_edges; e += p.TG)
+                lrow[e] = first ? (int8_t)0 : (int8_t)(64 - (int)((Lg[e] >> (8 * f)) & 0xFFu));
+        }
+        if (t == 0) {
+            const int s = (succ_mask >> f) & 1;
+            p.iters[frame] = it;
+            p.success[frame] = (uint8_t)s;
+            if (p.counters) {
+                atomicAdd(p.counters + 0, 1ull);
+                atomicAdd(p.counters + 1, (unsigned long long)s);
+                atomicAdd(p.counters + 4, (unsigned long long)it);
+            }
+        }
+    }
+}
+
+template <int DMAX, bool ESM>
+__global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1)
+    decode_kernel(const DecParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int2* s_layer = reinterpret_cast<int2*>(smem);
+    int2* s_edge = s_layer + p.Mb;
+    for (int i = threadIdx.x; i < p.Mb; i += blockDim.x) s_layer[i] = p.layer[i];
+    for (int i = threadIdx.x; i < p.nbase; i += blockDim.x) s_edge[i] = p.edge[i];
+    __syncthreads();
+
+    const int slot = threadIdx.x / p.TG;
+    const int t = threadIdx.x - slot * p.TG;
+    const int bar = 1 + slot;
+    unsigned char* gbase = smem + p.tab_bytes + (size_t)slot * p.group_bytes;
+    const long long gslot = (long long)blockIdx.x * p.GPC + slot;
+    uint32_t* E = ESM ? reinterpret_cast<uint32_t*>(gbase) : p.Ews + gslot * (long long)p.n;
+    uint8_t* sSyn = gbase + p.e_smem;
+    int* ctl = reinterpret_cast<int*>(sSyn + ((p.m + 15) & ~15));   // [0] group id, [1..2] flags
+    uint32_t* flags = reinterpret_cast<uint32_t*>(ctl + 1);
+    uint32_t* Lg = p.Lws + gslot * p.n_edges;
+
+    for (;;) {
+        if (t == 0) ctl[0] = atomicAdd(p.work, 1);
+        group_bar(bar, p.TG);
+        const long long g = *(volatile int*)&ctl[0];
+        if (g >= p.ngroups) break;
+        const long long f0 = g * kFramesPerGroup;
+        const int nl = (int)min((long long)kFramesPerGroup, p.F - f0);
+
+        // ---- E <- channel LLR, frame-interleaved, offset +128
+        if (p.vec_llr) {
+            const int n4 = p.n >> 2;
+            for (int q = t; q < n4; q += p.TG) {
+                uint32_t r[4];
+#pragma unroll
+                for (int f = 0; f < 4; ++f)
+                    r[f] = f < nl ? __ldcs(reinterpret_cast<const uint32_t*>(p.llr + (f0 + f) * p.n) + q) : 0x7F7F7F7Fu;
+                const uint32_t a = prmt(r[0], r[1], 0x5140u), b = prmt(r[2], r[3], 0x5140u);
+                const uint32_t c = prmt(r[0], r[1], 0x7362u), d = prmt(r[2], r[3], 0x7362u);
+                stE<ESM>(E, 4 * q + 0, prmt(a, b, 0x5410u) ^ 0x80808080u);
+                stE<ESM>(E, 4 * q + 1, prmt(a, b, 0x7632u) ^ 0x80808080u);
+                stE<ESM>(E, 4 * q + 2, prmt(c, d, 0x5410u) ^ 0x80808080u);
+                stE<ESM>(E, 4 * q + 3, prmt(c, d, 0x7632u) ^ 0x80808080u);
+            }
+        } else {
+            for (int j = t; j < p.n; j += p.TG) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    const uint32_t v = f < nl ? (uint8_t)p.llr[(f0 + f) * p.n + j] : 0x7Fu;
+                    w |= (v ^ 0x80u) << (8 * f);
+                }
+                stE<ESM>(E, j, w);
+            }
+        }
+        // ---- target syndrome: one nibble per check row (bit f = frame f)
+        for (int i8 = t; i8 < p.mb8; i8 += p.TG) {
+            uint32_t bf[4];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) bf[f] = f < nl ? p.syn[(f0 + f) * p.mb8 + i8] : 0u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = 8 * i8 + q;
+                if (i < p.m)
+                    sSyn[i] = (uint8_t)(((bf[0] >> q) & 1u) | (((bf[1] >> q) & 1u) << 1) |
+                                        (((bf[2] >> q) & 1u) << 2) | (((bf[3] >> q) & 1u) << 3));
+            }
+        }
+        if (t == 0) {
+            flags[0] = 0;
+            flags[1] = 0;
+        }
+        group_bar(bar, p.TG);
+
+        uint32_t active = (1u << nl) - 1u;
+        int chk = 0;
+        if (p.early_stop) {   // iteration-0 check (R10)
+            const uint32_t viol = syndrome_viol<ESM>(p, s_layer, s_edge, E, sSyn, t, flags, chk, bar);
+            const uint32_t done = active & ~viol;
+            if (done) {
+                finalize<ESM>(p, E, Lg, f0, done, 0, done, true, t);
+                group_bar(bar, p.TG);
+            }
+            active &= viol;
+        }
+        int it = 0;
+        while (active && it < p.T) {
+            ++it;
+            const bool first = it == 1;
+            for (int I = 0; I < p.Mb; ++I) {
+                const int2 li = s_layer[I];
+                layer_pass<DMAX, ESM>(p, li.x, s_edge + li.y, t, E, Lg + (long long)li.y * p.Z, sSyn + I * p.Z,
+                                      first);
+                group_bar(bar, p.TG);
+            }
+            if (p.early_stop) {
+                const uint32_t viol = syndrome_viol<ESM>(p, s_layer, s_edge, E, sSyn, t, flags, chk, bar);
+                const uint32_t done = active & ~viol;
+                if (done) {
+                    finalize<ESM>(p, E, Lg, f0, done, it, done, false, t);
+                    group_bar(bar, p.TG);
+                }
+                active &= viol;
+            }
+        }
+        if (active) {   // ran out of iterations (or early_stop = 0): state after sweep T (R12)
+            uint32_t succ = 0;
+            if (!p.early_stop) succ = active & ~syndrome_viol<ESM>(p, s_layer, s_edge, E, sSyn, t, flags, chk, bar);
+            finalize<ESM>(p, E, Lg, f0, active, it, succ, it == 0, t);
+        }
+        group_bar(bar, p.TG);
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// Alice's syndrome: one CTA per frame, frame bits staged in shared memory.
+// --------------------------------------------------------------------------------------
+__global__ void syndrome_kernel(const int2* __restrict__ layer, const int2* __restrict__ edge, int Mb, int Z,
+                                int n, int m, int nb8, int mb8, long long F, const uint8_t* __restrict__ bits,
+                                uint8_t* __restrict__ syn) {
+    extern __shared__ __align__(16) unsigned char sb[];
+    const int lane = threadIdx.x & 31;
+    for (long long f = blockIdx.x; f < F; f += gridDim.x) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < nb8; i += blockDim.x) sb[i] = bits[f * nb8 + i];
+        __syncthreads();
+        for (int iw = threadIdx.x & ~31; iw < m; iw += blockDim.x) {
+            const int i = iw + lane;
+            uint32_t par = 0;
+            if (i < m) {
+                const int I = i / Z, r = i - I * Z;
+                const int2 li = layer[I];
+                for (int k = 0; k < li.x; ++k) {
+                    const int2 e = edge[li.y + k];
+                    int idx = r + e.y;
+                    idx = idx >= Z ? idx - Z : idx;
+                    const int j = e.x + idx;
+                    par ^= (sb[j >> 3] >> (j & 7)) & 1u;
+                }
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, par != 0);
+            const int byte = (iw >> 3) + lane;
+            if (lane < 4 && byte < mb8) syn[f * mb8 + byte] = (uint8_t)(bal >> (8 * lane));
+        }
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// Bob's channel LLRs (P:103-112 quantization, P:157 puncture/shorten)
+// --------------------------------------------------------------------------------------
+__global__ void build_llr_kernel(int n, int nb8, long long F, int Lq, const uint8_t* __restrict__ y,
+                                 const uint8_t* __restrict__ known, const uint8_t* __restrict__ kind,
+                                 int8_t* __restrict__ llr) {
+    const long long total = F * nb8;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long f = q / nb8;
+        const int b = (int)(q - f * nb8);
+        const uint32_t yb = y[q];
+        const uint32_t kb = known ? known[q] : 0u;
+        int8_t* out = llr + f * n;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int j = 8 * b + s;
+            if (j >= n) break;
+            int v = ((yb >> s) & 1u) ? -Lq : Lq;
+            if (kind) {
+                const uint8_t kd = kind[j];
+                if (kd == 1) v = 0;
+                else if (kd == 2) v = ((kb >> s) & 1u) ? -127 : 127;
+            }
+            out[j] = (int8_t)v;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// scoring against Alice's key (harness)
+// --------------------------------------------------------------------------------------
+__global__ void score_kernel(int nb8, long long F, const uint8_t* __restrict__ bits, const uint8_t* __restrict__ x,
+                             const uint8_t* __restrict__ payload, const uint8_t* __restrict__ success,
+                             int32_t* __restrict__ errors, unsigned long long* counters) {
+    __shared__ int red[32];
+    for (long long f = blockIdx.x; f < F; f += gridDim.x) {
+        int c = 0;
+        for (int i = threadIdx.x; i < nb8; i += blockDim.x) {
+            uint32_t d = (uint32_t)(bits[f * nb8 + i] ^ x[f * nb8 + i]);
+            if (payload) d &= payload[i];
+            c += __popc(d);
+        }
+        c = __reduce_add_sync(0xffffffffu, c);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+            if (errors) errors[f] = tot;
+            if (counters && tot > 0) {
+                atomicAdd(counters + 2, 1ull);
+                if (success[f]) atomicAdd(counters + 3, 1ull);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void tau_table_kernel(uint8_t* out) {
+    const int p = threadIdx.x;   // 64 threads
+    for (int w = 0; w < 16; ++w) {
+        const uint32_t a = rep4((uint32_t)p);
+        const uint32_t b = (uint32_t)(4 * w) | ((uint32_t)(4 * w + 1) << 8) | ((uint32_t)(4 * w + 2) << 16) |
+                           ((uint32_t)(4 * w + 3) << 24);
+        const uint32_t t = tau4(a, b);
+        for (int q = 0; q < 4; ++q) out[p * 64 + 4 * w + q] = (uint8_t)(t >> (8 * q));
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// launch planning
+// --------------------------------------------------------------------------------------
+struct Plan {
+    int variant = 0;   // 1: DMAX 8 smem, 2: DMAX 20 smem, 3: generic smem, 4: generic global E
+    int TG = 0, GPC = 0, grid = 0, smem = 0, tab_bytes = 0, group_bytes = 0, e_smem = 0;
+    long long ngroups = 0, slots = 0;
+    size_t ws_L = 0, ws_E = 0, ws_total = 0;
+};
+
+struct DevInfo {
+    int sms = 0, smem_optin = 0;
+    bool ok = false;
+};
+
+DevInfo dev_info(int dev) {
+    static std::mutex mu;
+    static DevInfo cache[64];
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return DevInfo{};
+    if (!cache[dev].ok) {
+        cudaDeviceGetAttribute(&cache[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&cache[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cache[dev].ok = cache[dev].sms > 0;
+    }
+    return cache[dev];
+}
+
+template <int DMAX, bool ESM>
+const void* kfun() {
+    return reinterpret_cast<const void*>(&decode_kernel<DMAX, ESM>);
+}
+
+const void* kernel_of(int variant) {
+    switch (variant) {
+        case 1: return kfun<8, true>();
+        case 2: return kfun<20, true>();
+        case 3: return kfun<0, true>();
+        default: return kfun<0, false>();
+    }
+}
+
+int make_plan(const qkd_code* c, long long F, Plan& pl) {
+    int dev = 0;
+    QKD_CK(cudaGetDevice(&dev));
+    DevInfo di = dev_info(dev);
+    if (!di.ok) return fail(QKD_ECUDA, "cannot query device attributes");
+    pl.ngroups = (F + kFramesPerGroup - 1) / kFramesPerGroup;
+    pl.tab_bytes = (int)(((size_t)(c->Mb + c->nbase) * sizeof(int2) + 15) & ~size_t(15));
+    const int syn_bytes = (int)((c->m + 15) & ~15LL) + 16;
+    const long long e_bytes = 4LL * c->n;
+    const bool fits = pl.tab_bytes + e_bytes + syn_bytes <= di.smem_optin;
+    if (fits && c->maxdeg <= 8) pl.variant = 1;
+    else if (fits && c->maxdeg <= 20) pl.variant = 2;
+    else if (fits) pl.variant = 3;
+    else pl.variant = 4;
+    const int tg_max = pl.variant == 1 ? 1024 : (pl.variant == 2 ? 512 : 256);
+    pl.TG = (int)std::min<long long>(((long long)c->Z + 31) / 32 * 32, tg_max);
+    pl.e_smem = pl.variant == 4 ? 0 : (int)e_bytes;
+    pl.group_bytes = pl.e_smem + syn_bytes;
+    if (pl.tab_bytes + pl.group_bytes > di.smem_optin)
+        return fail(QKD_EUNSUP, "frame too long for the shared-memory syndrome buffer");
+    int gpc = std::min(15, tg_max / pl.TG);
+    gpc = std::min<int>(gpc, (di.smem_optin - pl.tab_bytes) / pl.group_bytes);
+    const long long need = (pl.ngroups + di.sms - 1) / di.sms;
+    gpc = (int)std::max<long long>(1, std::min<long long>(gpc, need));
+    pl.GPC = gpc;
+    pl.smem = pl.tab_bytes + gpc * pl.group_bytes;
+    const void* k = kernel_of(pl.variant);
+    QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+    int per_sm = 0;
+    QKD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.TG * pl.GPC, pl.smem));
+    if (per_sm < 1) return fail(QKD_EUNSUP, "decode kernel cannot be resident with this geometry");
+    const long long ctas = (pl.ngroups + gpc - 1) / gpc;
+    pl.grid = (int)std::max<long long>(1, std::min<long long>(ctas, (long long)per_sm * di.sms));
+    pl.slots = (long long)pl.grid * gpc;
+    pl.ws_L = (size_t)pl.slots * (size_t)c->n_edges * 4;
+    pl.ws_E = pl.variant == 4 ? (size_t)pl.slots * (size_t)c->n * 4 : 0;
+    pl.ws_total = 256 + pl.ws_L + pl.ws_E;
+    return QKD_OK;
+}
+
+}  // namespace
+
+// ======================================================================================
+// C ABI
+// ======================================================================================
+extern "C" {
+
+const char* qkd_last_error(void) { return g_err.c_str(); }
+
+int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t Z, const uint8_t* pos_kind,
+                    qkd_code** out) {
+    if (!out || !base_shifts) return fail(QKD_EINVAL, "null argument");
+    *out = nullptr;
+    if (Mb < 1 || Nb <= Mb || Z < 1) return fail(QKD_EINVAL, "need Mb >= 1, Nb > Mb, Z >= 1");
+    if ((long long)Nb * Z > (1LL << 30)) return fail(QKD_EUNSUP, "n too large");
+    qkd_code* c = new qkd_code();
+    c->Mb = Mb;
+    c->Nb = Nb;
+    c->Z = Z;
+    c->n = (int64_t)Nb * Z;
+    c->m = (int64_t)Mb * Z;
+    for (int I = 0; I < Mb; ++I) {
+        int2 li = make_int2(0, (int)c->edge.size());
+        for (int J = 0; J < Nb; ++J) {
+            const int s = base_shifts[(size_t)I * Nb + J];
+            if (s < -1 || s >= Z) {
+                delete c;
+                return fail(QKD_ESHIFT, "shift " + std::to_string(s) + " at base block (" + std::to_string(I) +
+                                            "," + std::to_string(J) + ") outside [-1, Z)");
+            }
+            if (s >= 0) {
+                c->edge.push_back(make_int2(J * Z, s));
+                li.x++;
+            }
+        }
+        if (li.x > 64) {
+            delete c;
+            return fail(QKD_EUNSUP, "check degree > 64 in block row " + std::to_string(I));
+        }
+        c->maxdeg = std::max(c->maxdeg, li.x);
+        c->layer.push_back(li);
+    }
+    c->nbase = (int)c->edge.size();
+    c->n_edges = (int64_t)c->nbase * Z;
+    cudaError_t e = cudaGetDevice(&c->device);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_layer, sizeof(int2) * c->layer.size());
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_edge, sizeof(int2) * std::max<size_t>(1, c->edge.size()));
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_layer, c->layer.data(), sizeof(int2) * c->layer.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !c->edge.empty())
+        e = cudaMemcpy(c->d_edge, c->edge.data(), sizeof(int2) * c->edge.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && pos_kind) {
+        bool any = false;
+        std::vector<uint8_t> pay((size_t)(c->n + 7) / 8, 0);
+        for (int64_t j = 0; j < c->n; ++j) {
+            if (pos_kind[j] > 2) {
+                qkd_code_destroy(c);
+                return fail(QKD_EINVAL, "pos_kind values must be 0, 1 or 2");
+            }
+            if (pos_kind[j] != 0) any = true;
+            if (pos_kind[j] == 2) c->has_short = true;
+            if (pos_kind[j] == 0) pay[j >> 3] |= (uint8_t)(1u << (j & 7));
+        }
+        if (any) {
+            e = cudaMalloc(&c->d_kind, (size_t)c->n);
+            if (e == cudaSuccess) e = cudaMemcpy(c->d_kind, pos_kind, (size_t)c->n, cudaMemcpyHostToDevice);
+            if (e == cudaSuccess) e = cudaMalloc(&c->d_payload, pay.size());
+            if (e == cudaSuccess) e = cudaMemcpy(c->d_payload, pay.data(), pay.size(), cudaMemcpyHostToDevice);
+        }
+    }
+    if (e != cudaSuccess) {
+        qkd_code_destroy(c);
+        return fail(e == cudaErrorMemoryAllocation ? QKD_ENOMEM : QKD_ECUDA,
+                    std::string("code tables: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return QKD_OK;
+}
+
+void qkd_code_destroy(qkd_code* c) {
+    if (!c) return;
+    if (c->d_layer) cudaFree(c->d_layer);
+    if (c->d_edge) cudaFree(c->d_edge);
+    if (c->d_kind) cudaFree(c->d_kind);
+    if (c->d_payload) cudaFree(c->d_payload);
+    delete c;
+}
+
+int qkd_code_info(const qkd_code* c, int64_t* n, int64_t* m, int64_t* n_edges, int32_t* max_row_deg) {
+    if (!c) return fail(QKD_EINVAL, "null code");
+    if (n) *n = c->n;
+    if (m) *m = c->m;
+    if (n_edges) *n_edges = c->n_edges;
+    if (max_row_deg) *max_row_deg = c->maxdeg;
+    return QKD_OK;
+}
+
+int qkd_llr_magnitude(double q) {
+    if (!(q > 0.0 && q < 0.5)) return fail(QKD_EINVAL, "qber must lie in (0, 0.5)");
+    const double v = std::nearbyint(4.0 * std::log((1.0 - q) / q));   // ties never occur at the configs
+    return (int)std::min(127.0, v);
+}
+
+int qkd_syndrome(const qkd_code* c, int64_t F, const uint8_t* bits, uint8_t* syn, void* stream) {
+    if (!c || F < 0 || (F > 0 && (!bits || !syn))) return fail(QKD_EINVAL, "bad argument");
+    if (F == 0) return QKD_OK;
+    const int nb8 = (int)((c->n + 7) / 8), mb8 = (int)((c->m + 7) / 8);
+    if (nb8 > 160 * 1024) return fail(QKD_EUNSUP, "frame too long for the syndrome kernel");
+    int dev = 0;
+    QKD_CK(cudaGetDevice(&dev));
+    const DevInfo di = dev_info(dev);
+    QKD_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(&syndrome_kernel),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, nb8));
+    const int grid = (int)std::min<long long>(F, (long long)di.sms * 8);
+    syndrome_kernel<<<grid, 256, nb8, (cudaStream_t)stream>>>(c->d_layer, c->d_edge, c->Mb, c->Z, (int)c->n,
+                                                               (int)c->m, nb8, mb8, F, bits, syn);
+    QKD_CK(cudaGetLastError());
+    return QKD_OK;
+}
+
+int qkd_build_llr(const qkd_code* c, double qber, int64_t F, const uint8_t* y, const uint8_t* known, int8_t* llr,
+                  void* stream) {
+    if (!c || F < 0 || (F > 0 && (!y || !llr))) return fail(QKD_EINVAL, "bad argument");
+    const int Lq = qkd_llr_magnitude(qber);
+    if (Lq < 0) return Lq;
+    if (c->has_short && !known) return fail(QKD_EINVAL, "code has shortened positions: known_bits required");
+    if (F == 0) return QKD_OK;
+    const int nb8 = (int)((c->n + 7) / 8);
+    const long long total = F * nb8;
+    const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 64);
+    build_llr_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((int)c->n, nb8, F, Lq, y, c->d_kind ? known : nullptr,
+                                                             c->d_kind, llr);
+    QKD_CK(cudaGetLastError());
+    return QKD_OK;
+}
+
+size_t qkd_workspace_bytes(const qkd_code* c, int64_t F) {
+    if (!c || F < 0) return 0;
+    Plan pl;
+    if (make_plan(c, std::max<int64_t>(F, 1), pl) != QKD_OK) return 0;
+    return pl.ws_total;
+}
+
+int qkd_launch_info(const qkd_code* c, int64_t F, int32_t* info) {
+    if (!c || !info || F < 1) return fail(QKD_EINVAL, "bad argument");
+    Plan pl;
+    const int rc = make_plan(c, F, pl);
+    if (rc) return rc;
+    info[0] = pl.variant;
+    info[1] = pl.TG;
+    info[2] = pl.GPC;
+    info[3] = pl.grid;
+    info[4] = pl.smem;
+    info[5] = kFramesPerGroup;
+    info[6] = (int32_t)pl.ngroups;
+    return QKD_OK;
+}
+
+int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint8_t* syn, int32_t max_iter,
+                     int32_t early_stop, void* ws, size_t ws_bytes, uint8_t* bits, int32_t* iters,
+                     uint8_t* success, int8_t* fL, int8_t* fE, int64_t* counters, void* stream) {
+    if (!c || F < 0 || max_iter < 0) return fail(QKD_EINVAL, "bad argument");
+    if (F == 0) return QKD_OK;
+    if (!llr || !syn || !ws || !bits || !iters || !success) return fail(QKD_EINVAL, "null buffer");
+    Plan pl;
+    int rc = make_plan(c, F, pl);
+    if (rc) return rc;
+    if (ws_bytes < pl.ws_total)
+        return fail(QKD_EDIM, "workspace too small: need " + std::to_string(pl.ws_total) + " bytes");
+    char* w = static_cast<char*>(ws);
+    DecParams p{};
+    p.layer = c->d_layer;
+    p.edge = c->d_edge;
+    p.Mb = c->Mb;
+    p.Z = c->Z;
+    p.nbase = c->nbase;
+    p.n = (int)c->n;
+    p.m = (int)c->m;
+    p.mb8 = (int)((c->m + 7) / 8);
+    p.nb8 = (int)((c->n + 7) / 8);
+    p.n_edges = c->n_edges;
+    p.llr = llr;
+    p.syn = syn;
+    p.F = F;
+    p.ngroups = pl.ngroups;
+    p.T = max_iter;
+    p.early_stop = early_stop ? 1 : 0;
+    p.vec_llr = (c->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(llr) & 3) == 0);
+    p.work = reinterpret_cast<int*>(w);
+    p.Lws = reinterpret_cast<uint32_t*>(w + 256);
+    p.Ews = pl.ws_E ? reinterpret_cast<uint32_t*>(w + 256 + pl.ws_L) : nullptr;
+    p.bits = bits;
+    p.iters = iters;
+    p.success = success;
+    p.fL = fL;
+    p.fE = fE;
+    p.counters = reinterpret_cast<unsigned long long*>(counters);
+    p.TG = pl.TG;
+    p.GPC = pl.GPC;
+    p.tab_bytes = pl.tab_bytes;
+    p.group_bytes = pl.group_bytes;
+    p.e_smem = pl.e_smem;
+    cudaStream_t st = (cudaStream_t)stream;
+    QKD_CK(cudaMemsetAsync(p.work, 0, sizeof(int), st));
+    const dim3 grid(pl.grid), block(pl.TG * pl.GPC);
+    switch (pl.variant) {
+        case 1: decode_kernel<8, true><<<grid, block, pl.smem, st>>>(p); break;
+        case 2: decode_kernel<20, true><<<grid, block, pl.smem, st>>>(p); break;
+        case 3: decode_kernel<0, true><<<grid, block, pl.smem, st>>>(p); break;
+        default: decode_kernel<0, false><<<grid, block, pl.smem, st>>>(p); break;
+    }
+    QKD_CK(cudaGetLastError());
+    return QKD_OK;
+}
+
+int qkd_score_batch(const qkd_code* c, int64_t F, const uint8_t* bits, const uint8_t* x, const uint8_t* success,
+                    int32_t* errors, int64_t* counters, void* stream) {
+    if (!c || F < 0 || (F > 0 && (!bits || !x || !success))) return fail(QKD_EINVAL, "bad argument");
+    if (F == 0) return QKD_OK;
+    const int nb8 = (int)((c->n + 7) / 8);
+    const int grid = (int)std::min<long long>(F, 148LL * 16);
+    score_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(nb8, F, bits, x, c->d_payload, success, errors,
+                                                         reinterpret_cast<unsigned long long*>(counters));
+    QKD_CK(cudaGetLastError());
+    return QKD_OK;
+}
+
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+size_t qkd_reconcile_device_bytes(const qkd_code* c, int64_t F) {
+    if (!c || F < 0) return 0;
+    const size_t nb8 = (size_t)((c->n + 7) / 8), mb8 = (size_t)((c->m + 7) / 8);
+    size_t s = 0;
+    s += align256(F * nb8);                   // Bob's bits
+    s += c->has_short ? align256(F * nb8) : 0;   // known bits
+    s += align256(F * mb8);                   // syndrome
+    s += align256(F * (size_t)c->n);          // llr
+    s += align256(F * nb8);                   // bits out
+    s += align256(F * 4);                     // iters
+    s += align256(F);                         // success
+    return s + align256(qkd_workspace_bytes(c, F));
+}
+
+int qkd_reconcile_host(const qkd_code* c, double qber, int64_t F, const uint8_t* y_h, const uint8_t* known_h,
+                       const uint8_t* syn_h, int32_t max_iter, int32_t early_stop, void* dbuf, size_t dbytes,
+                       uint8_t* bits_h, int32_t* iters_h, uint8_t* succ_h, void* stream) {
+    if (!c || F < 0) return fail(QKD_EINVAL, "bad argument");
+    if (F == 0) return QKD_OK;
+    if (!y_h || !syn_h || !bits_h || !iters_h || !succ_h || !dbuf) return fail(QKD_EINVAL, "null buffer");
+    if (c->has_short && !known_h) return fail(QKD_EINVAL, "known bits required (shortened positions)");
+    const size_t need = qkd_reconcile_device_bytes(c, F);
+    if (need == 0 || dbytes < need) return fail(QKD_EDIM, "device buffer too small: need " + std::to_string(need));
+    const size_t nb8 = (size_t)((c->n + 7) / 8), mb8 = (size_t)((c->m + 7) / 8);
+    char* w = static_cast<char*>(dbuf);
+    uint8_t* d_y = (uint8_t*)w; w += align256(F * nb8);
+    uint8_t* d_k = nullptr;
+    if (c->has_short) { d_k = (uint8_t*)w; w += align256(F * nb8); }
+    uint8_t* d_s = (uint8_t*)w; w += align256(F * mb8);
+    int8_t* d_llr = (int8_t*)w; w += align256(F * (size_t)c->n);
+    uint8_t* d_b = (uint8_t*)w; w += align256(F * nb8);
+    int32_t* d_it = (int32_t*)w; w += align256(F * 4);
+    uint8_t* d_su = (uint8_t*)w; w += align256(F);
+    const size_t wsb = qkd_workspace_bytes(c, F);
+    cudaStream_t st = (cudaStream_t)stream;
+    QKD_CK(cudaMemcpyAsync(d_y, y_h, F * nb8, cudaMemcpyHostToDevice, st));
+    if (d_k) QKD_CK(cudaMemcpyAsync(d_k, known_h, F * nb8, cudaMemcpyHostToDevice, st));
+    QKD_CK(cudaMemcpyAsync(d_s, syn_h, F * mb8, cudaMemcpyHostToDevice, st));
+    int rc = qkd_build_llr(c, qber, F, d_y, d_k, d_llr, stream);
+    if (rc) return rc;
+    rc = qkd_decode_batch(c, F, d_llr, d_s, max_iter, early_stop, w, wsb, d_b, d_it, d_su, nullptr, nullptr, nullptr,
+                          stream);
+    if (rc) return rc;
+    QKD_CK(cudaMemcpyAsync(bits_h, d_b, F * nb8, cudaMemcpyDeviceToHost, st));
+    QKD_CK(cudaMemcpyAsync(iters_h, d_it, F * 4, cudaMemcpyDeviceToHost, st));
+    QKD_CK(cudaMemcpyAsync(succ_h, d_su, F, cudaMemcpyDeviceToHost, st));
+    QKD_CK(cudaStreamSynchronize(st));
+    return QKD_OK;
+}
+
+int qkd_tau_table(uint8_t* out, void* stream) {
+    if (!out) return fail(QKD_EINVAL, "null buffer");
+    tau_table_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(out);
+    QKD_CK(cudaGetLastError());
+    return QKD_OK;
+}
+
+}  // extern "C"

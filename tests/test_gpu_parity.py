@@ -1,0 +1,179 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit for bit, on
+the same seeded inputs.  The decoder is integer-only, so every output --
+hard decisions, iteration counts, success flags and the final int8 message state L and E --
+must be identical."""
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from _common import assert_same, gpu_decode, oracle_decode, to_np, workload_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tau_table_exhaustive(gpu):
+    t = gpu.tau_table().cpu().numpy()
+    ref = np.array([[oracle.tau(p, q) for q in range(64)] for p in range(64)], dtype=np.uint8)
+    assert np.array_equal(t, ref)
+
+
+@pytest.mark.parametrize("name,F", [("C1", 64), ("C2", 64), ("C3", 8), ("C4@0.02", 4)])
+def test_syndrome_and_llr_parity(gpu, name, F):
+    import torch
+
+    w, shifts, kind, x, y, llr, syn = workload_inputs(name, F)
+    code = gpu.QCCode(shifts, w.Z, kind)
+    xs = torch.from_numpy(x).cuda()
+    ys = torch.from_numpy(y).cuda()
+    s_gpu = code.syndrome(xs).cpu().numpy()
+    assert np.array_equal(s_gpu, syn)
+    l_gpu = code.build_llr(w.qber, ys, xs if kind is not None else None).cpu().numpy()
+    assert np.array_equal(l_gpu, llr)
+
+
+@pytest.mark.parametrize("name,F", [("C1", 64), ("C2", 192), ("C3", 12), ("C4@0.01", 4), ("C4@0.02", 4),
+                                    ("C4@0.04", 4), ("C4@0.06", 4), ("C4@0.08", 4)])
+def test_decode_parity_workloads(gpu, name, F):
+    w, shifts, kind, x, y, llr, syn = workload_inputs(name, F)
+    g, code = gpu_decode(gpu, shifts, w.Z, kind, llr, syn, w.max_iter, w.early_stop)
+    o = oracle_decode(shifts, w.Z, llr, syn, w.max_iter, w.early_stop)
+    assert_same(g, o)
+
+
+def _tiny_cases():
+    rng = np.random.default_rng(11)
+    cases = {}
+    cases["2x4_Z5"] = (np.array([[0, 1, 3, -1], [2, -1, 4, 0]]), 5)                # Z not pow2, Z < 32
+    cases["2x3_Z7_n21"] = (np.array([[0, 3, 5], [6, -1, 1]]), 7)                   # n % 4 != 0
+    cases["deg1_deg2"] = (np.array([[0, -1, -1, -1], [3, 1, -1, -1], [2, 0, 4, 1]]), 6)
+    sh = rng.integers(0, 40, (3, 30))
+    sh[1, rng.random(30) < 0.5] = -1
+    sh[2, rng.random(30) < 0.8] = -1
+    cases["deg30_generic"] = (sh, 40)                                              # degree > 20
+    sh = rng.integers(0, 64, (4, 24))
+    sh[rng.random((4, 24)) < 0.4] = -1
+    cases["deg9to20"] = (sh, 64)
+    sh = rng.integers(0, 96, (3, 9))
+    cases["Z96_multiwarp"] = (sh, 96)                                              # Z%32==0, not pow2
+    return cases
+
+
+TINY = _tiny_cases()
+
+
+@pytest.mark.parametrize("case", sorted(TINY))
+@pytest.mark.parametrize("F", [1, 3, 7, 13])
+@pytest.mark.parametrize("early_stop", [1, 0])
+def test_decode_parity_edge_cases(gpu, case, F, early_stop):
+    """Random full-range LLRs (saturated +-127, zeros, everything in between) and random
+    target syndromes exercise the saturation guard, the 6-bit clamp, x = 0 ties and
+    non-convergence; ragged batches exercise the padded frame lanes."""
+    shifts, Z = TINY[case]
+    shifts = np.asarray(shifts, dtype=np.int32)
+    Mb, Nb = shifts.shape
+    n, m = Nb * Z, Mb * Z
+    rng = np.random.default_rng(zlib.crc32(f"{case}/{F}/{early_stop}".encode()))
+    special = rng.choice(np.array([-127, -126, -64, -63, -20, -5, -1, 0, 1, 4, 17, 63, 64, 100, 126, 127]),
+                         size=(F, n))
+    uniform = rng.integers(-127, 128, size=(F, n))
+    llr = np.where(rng.random((F, n)) < 0.5, special, uniform).astype(np.int8)
+    syn = rng.integers(0, 256, size=(F, (m + 7) // 8), dtype=np.uint8)
+    for T in (0, 1, 9):
+        g, _ = gpu_decode(gpu, shifts, Z, None, llr, syn, T, early_stop)
+        o = oracle_decode(shifts, Z, llr, syn, T, early_stop)
+        assert_same(g, o)
+
+
+def test_decode_parity_channel_frames_tiny(gpu):
+    """Many channel-like frames on a tiny code (mix of convergence iterations)."""
+    shifts, Z = TINY["2x4_Z5"]
+    code = oracle.Code(shifts, Z)
+    x, y, _ = synth.frames(code.n, 0.07, 99, 0, 997)
+    syn = code.syndrome(x)
+    llr = code.build_llr(0.07, y)
+    g, _ = gpu_decode(gpu, shifts, Z, None, llr, syn, 25, 1)
+    o = oracle_decode(shifts, Z, llr, syn, 25, 1)
+    assert_same(g, o)
+    assert len(np.unique(o["iters"])) > 3
+
+
+def test_zero_error_frames_iteration_zero(gpu):
+    w, shifts, kind, x, y, llr, syn = workload_inputs("C2", 9)
+    oc = oracle.Code(shifts, w.Z)
+    llr0 = oc.build_llr(w.qber, x)
+    g, _ = gpu_decode(gpu, shifts, w.Z, None, llr0, syn, w.max_iter, 1)
+    assert (g["iters"] == 0).all() and (g["success"] == 1).all()
+    assert np.array_equal(g["bits"], x)
+    assert not g["L"].any()
+
+
+def test_batch_composition_invariance(gpu):
+    """a frame's result does not depend on the batch around it."""
+    w, shifts, kind, x, y, llr, syn = workload_inputs("C2", 40)
+    full, _ = gpu_decode(gpu, shifts, w.Z, None, llr, syn, w.max_iter, 1)
+    for a, b in ((0, 1), (3, 11), (17, 40), (5, 6)):
+        part, _ = gpu_decode(gpu, shifts, w.Z, None, llr[a:b], syn[a:b], w.max_iter, 1)
+        for k in full:
+            assert np.array_equal(full[k][a:b], part[k]), (k, a, b)
+
+
+def test_counters_and_score(gpu):
+    import torch
+
+    w, shifts, kind, x, y, llr, syn = workload_inputs("C2", 128)
+    counters = torch.zeros(5, dtype=torch.int64, device="cuda")
+    code = gpu.QCCode(shifts, w.Z, kind)
+    r = code.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(syn).cuda(), w.max_iter, True,
+                    counters=counters)
+    errs = code.score(r["bits"], torch.from_numpy(x).cuda(), r["success"], counters=counters, want_errors=True)
+    c = counters.cpu().numpy()
+    o = oracle_decode(shifts, w.Z, llr, syn, w.max_iter, 1, want_state=False)
+    ob = np.unpackbits(o["bits"] ^ x, axis=1, bitorder="little")[:, : w.n].sum(1)
+    assert np.array_equal(errs.cpu().numpy(), ob)
+    assert c[0] == 128 and c[1] == o["success"].sum() and c[4] == o["iters"].sum()
+    assert c[2] == (ob > 0).sum() and c[3] == ((ob > 0) & (o["success"] == 1)).sum()
+
+
+def test_reconcile_host_matches_device_path(gpu):
+    import torch
+
+    w, shifts, kind, x, y, llr, syn = workload_inputs("C4@0.04", 4)
+    code = gpu.QCCode(shifts, w.Z, kind)
+    bits, iters, succ = code.reconcile_host(w.qber, y, syn, w.max_iter, True, known_bits=x)
+    o = oracle_decode(shifts, w.Z, llr, syn, w.max_iter, 1, want_state=False)
+    assert np.array_equal(bits, o["bits"]) and np.array_equal(iters, o["iters"])
+    assert np.array_equal(succ, o["success"])
+
+
+@pytest.mark.parametrize("name", ["C5b", "C5a"])
+def test_full_size_sampled(gpu, name):
+    """BASELINE configs[4] at full size (65536 frames) in the bench's launch configuration;
+    sampled frames against the oracle one by one, plus success => syndrome match on a
+    4096-frame slice checked by the oracle's own syndrome."""
+    import torch
+
+    w = synth.workload(name)
+    F = w.frames
+    shifts = w.shifts()
+    x, y, _ = w.gen(0, F)
+    code = gpu.QCCode(shifts, w.Z)
+    xs = torch.from_numpy(x).cuda()
+    syn = code.syndrome(xs)
+    llr = code.build_llr(w.qber, torch.from_numpy(y).cuda())
+    r = to_np(code.decode(llr, syn, w.max_iter, True))
+    oc = oracle.Code(shifts, w.Z)
+    rng = np.random.default_rng(5)
+    sample = np.unique(np.concatenate([[0, 1, 2, 3, F - 1], rng.integers(0, F, 11)]))
+    xo, yo = x[sample], y[sample]
+    so = oc.syndrome(xo)
+    assert np.array_equal(so, syn.cpu().numpy()[sample])
+    o = oc.decode(oc.build_llr(w.qber, yo), so, w.max_iter, 1, want_state=False)
+    for k in ("bits", "iters", "success"):
+        assert np.array_equal(r[k][sample], o[k]), k
+    sl = slice(F - 4096, F)
+    s_bits = oc.syndrome(r["bits"][sl])
+    ok = r["success"][sl] == 1
+    assert np.array_equal(s_bits[ok], syn.cpu().numpy()[sl][ok])
