@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark: corrected-key Mbps of the batched quantized LDPC syndrome decoder on B200.
+
+Workload (BASELINE.json configs[4], "C5"): 65536 frames of the config-3 code (n=51200,
+R~0.84, QBER 2%) plus 65536 frames of the config-2 code (n=8192, R=0.5, QBER 8%), split
+evenly across ranks by global frame id (strong scaling), max 50 iterations, early stop.
+One step = for both workloads: Alice's syndrome, Bob's int8 LLRs, the fused layered
+decode, scoring against Alice's key (counters) -- then one NCCL allreduce of the int64
+counters when N > 1.  Inputs are synthetic (synth/, seeded BSC frames on seeded QC codes).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload C5|C1|..]
+
+--impl reference times the CPU oracle (the reference arm of this tier; oracle/) on a bounded
+sample per step on the host cores and extrapolates to the same workload and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "corrected-key Mbps at QBER 1-8% (1/2/4/8 GPU); % of HBM roofline per iteration"
+UNIT = "Mbps"
+WORKLOADS = {"C5": ["C5a", "C5b"], "C1": ["C1"], "C2": ["C2"], "C3": ["C3"],
+             "C4": [f"C4@{q:g}" for q in synth.C4_QBERS]}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def payload_bits(w):
+    d, p, s = w.rate_adaptive_counts()
+    return w.n - p - s
+
+
+# ------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------- oracle arm
+def oracle_sample(names, frames_per, nthreads):
+    """Decode a bounded sample with the CPU oracle.  Returns per-workload dicts with the
+    wall time, frames, corrected frames."""
+    import oracle
+
+    out = {}
+    for name in names:
+        w = synth.workload(name)
+        F = frames_per[name]
+        x, y, _ = w.gen(0, F, nthreads)
+        kind = w.pos_kind()
+        oc = oracle.Code(w.shifts(), w.Z)
+        syn = oc.syndrome(x)
+        t0 = time.perf_counter()
+        llr = oc.build_llr(w.qber, y, kind, x)
+        r = oc.decode(llr, syn, w.max_iter, w.early_stop, want_state=False, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+        ok = (r["success"] == 1) & (r["bits"] == x).all(axis=1) if kind is None else (r["success"] == 1) & (
+            ((r["bits"] ^ x) & np.packbits(kind == 0, bitorder="little")[None, :]) == 0).all(axis=1)
+        out[name] = dict(seconds=dt, frames=F, corrected=int(ok.sum()), iters=float(r["iters"].mean()))
+    return out
+
+
+def extrapolate(names, sample, frames_total):
+    """Corrected-key Mbps of the whole step (all workloads, full frame counts) from the sample."""
+    bits = 0.0
+    secs = 0.0
+    for name in names:
+        w = synth.workload(name)
+        s = sample[name]
+        per_frame = s["seconds"] / s["frames"]
+        secs += per_frame * frames_total[name]
+        bits += (s["corrected"] / s["frames"]) * frames_total[name] * payload_bits(w)
+    return bits / secs / 1e6, secs
+
+
+def default_sample(names, cores):
+    per = {}
+    for name in names:
+        w = synth.workload(name)
+        edges_iter = w.max_iter * (w.shifts() >= 0).sum() * w.Z       # worst-case work per frame
+        # ~3e7 scalar edge updates per second per core for the plain -O2 oracle
+        per_frame_s = edges_iter / 3e7
+        per[name] = int(max(cores, min(w.frames, cores * max(1, round(4.0 / per_frame_s)))))
+    return per
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    names = WORKLOADS[args.workload]
+    cores = host_cores()
+    frames_total = {n: synth.workload(n).frames for n in names}
+    per = default_sample(names, cores)
+    per = {k: max(1, v // 4) for k, v in per.items()}          # ~1 s of CPU per step
+    vals, secs = [], []
+    for i in range(args.warmup + args.steps):
+        s = oracle_sample(names, per, cores)
+        v, _ = extrapolate(names, s, frames_total)
+        if i >= args.warmup:
+            vals.append(v)
+            secs.append(sum(x["seconds"] for x in s.values()))
+    value = statistics.median(vals)
+    sample_desc = ", ".join(f"first {per[n]} frames of {n}" for n in names)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic", "config": workload_config(args.workload),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample_desc + " per step, extrapolated to the full workload"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(wl):
+    names = WORKLOADS[wl]
+    cfg = {"workload": wl + " = " + " + ".join(
+        f"{n}({synth.workload(n).Mb}x{synth.workload(n).Nb} Z={synth.workload(n).Z} n={synth.workload(n).n} "
+        f"QBER={synth.workload(n).qber:g} frames={synth.workload(n).frames} T={synth.workload(n).max_iter})"
+        for n in names),
+        "frames_per_workload": {n: synth.workload(n).frames for n in names},
+        "max_iter": {n: synth.workload(n).max_iter for n in names},
+        "early_stop": True, "frames_per_group": 4,
+        "l2": "inputs larger than L2 (C5a LLR alone is 3.4 GB); no flush needed"}
+    return cfg
+
+
+# ------------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1903_10107_b200 as qkd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    names = WORKLOADS[args.workload]
+    nthreads = max(1, host_cores() // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+
+    # ---- per-workload state (this rank's shard of global frame ids)
+    W = []
+    for name in names:
+        w = synth.workload(name)
+        F = w.frames
+        a, b = rank * F // world, (rank + 1) * F // world
+        t0 = time.perf_counter()
+        x, y, _ = w.gen(a, b - a, nthreads)
+        kind = w.pos_kind()
+        code = qkd.QCCode(w.shifts(), w.Z, kind)
+        Fr = b - a
+        st = dict(name=name, w=w, code=code, F=Fr, x_host=x, y_host=y,
+                  x=torch.from_numpy(x).to(dev), y=torch.from_numpy(y).to(dev))
+        st["syn"] = torch.empty((Fr, code.mb8), dtype=torch.uint8, device=dev)
+        st["llr"] = torch.empty((Fr, code.n), dtype=torch.int8, device=dev)
+        st["ws"] = torch.empty(code.workspace_bytes(Fr), dtype=torch.uint8, device=dev)
+        st["out"] = dict(bits=torch.empty((Fr, code.nb8), dtype=torch.uint8, device=dev),
+                         iters=torch.empty(Fr, dtype=torch.int32, device=dev),
+                         success=torch.empty(Fr, dtype=torch.uint8, device=dev))
+        st["info"] = code.launch_info(Fr)
+        st["known"] = st["x"] if kind is not None else None
+        log(f"[rank {rank}] {name}: frames [{a},{b}) generated in {time.perf_counter() - t0:.1f}s, "
+            f"launch {st['info']}")
+        W.append(st)
+    counters = torch.zeros((len(W), 5), dtype=torch.int64, device=dev)
+    ev = {s["name"]: [] for s in W}
+
+    def step(record):
+        counters.zero_()
+        for i, s in enumerate(W):
+            code = s["code"]
+            code.syndrome(s["x"], out=s["syn"])                       # Alice (a3)
+            code.build_llr(s["w"].qber, s["y"], s["known"], out=s["llr"])   # Bob (a2)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            code.decode(s["llr"], s["syn"], s["w"].max_iter, True, counters=counters[i], workspace=s["ws"],
+                        out=s["out"])                                  # a4-a8
+            e1.record(stream)
+            if record:
+                ev[s["name"]].append((e0, e1))
+            code.score(s["out"]["bits"], s["x"], s["out"]["success"], counters=counters[i])   # a9
+        if world > 1:
+            dist.all_reduce(counters)                                 # a9: the only collective
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    for v in ev.values():
+        v.clear()
+    clk = ClockSampler(local)
+    clk.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms_local = t_start.elapsed_time(t_end)
+    ms = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_total = float(ms.item())
+    c = counters.cpu().numpy()      # last step (identical every step)
+
+    # ---- metric: corrected = syndrome matched and no payload bit error
+    corrected_bits = sum(int(c[i, 1] - c[i, 3]) * payload_bits(s["w"]) for i, s in enumerate(W))
+    processed_bits = sum(int(c[i, 0]) * payload_bits(s["w"]) for i, s in enumerate(W))
+    sec_per_step = ms_total / 1000.0 / args.steps
+    value = corrected_bits / sec_per_step / 1e6
+    processed = processed_bits / sec_per_step / 1e6
+
+    # ---- roofline of the decode kernel (algorithmic bytes per launch / event time)
+    peak, peak_kind = peaks()
+    dec_ms = 0.0
+    alg_bytes = 0.0
+    per_wl = {}
+    for i, s in enumerate(W):
+        code = s["code"]
+        t = statistics.mean(a.elapsed_time(b) for a, b in ev[s["name"]])
+        # this rank's bytes: iterations actually run by its frames (counters are global)
+        frames_g, iters_g = int(c[i, 0]), int(c[i, 4])
+        frac = s["F"] / max(1, frames_g)
+        b_it = 2 * code.n_edges
+        once = code.n + code.mb8 + code.nb8 + 5
+        bytes_rank = frac * (iters_g * b_it + frames_g * once)
+        dec_ms += t
+        alg_bytes += bytes_rank
+        per_wl[s["name"]] = {"decode_ms": t, "frames": frames_g, "fer": 1 - c[i, 1] / max(1, frames_g),
+                             "mean_iters": iters_g / max(1, frames_g), "undetected": int(c[i, 3]),
+                             "frames_with_errors": int(c[i, 2]),
+                             "alg_GBps": bytes_rank / (t / 1000) / 1e9,
+                             "launch": s["info"]}
+    achieved = alg_bytes / (dec_ms / 1000.0) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get("decode_dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # ---- end to end through the C ABI with host buffers (pinned), N GPUs
+    e2e = run_e2e(args, W, world, rank, dev)
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cores = host_cores()
+            per = default_sample(names, cores)
+            t0 = time.perf_counter()
+            sm = oracle_sample(names, per, cores)
+            v, _ = extrapolate(names, sm, {n: synth.workload(n).frames for n in names})
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": ", ".join(f"first {per[n]} frames of {n}" for n in names)
+                   + f" ({time.perf_counter() - t0:.1f}s of CPU work), extrapolated to the full workload"}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+                "config": dict(workload_config(args.workload), parallelism=f"frames sharded over {world} rank(s)",
+                               processed_key_mbps=processed, per_workload=per_wl),
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "kernel": "decode_kernel (both workloads, per-step sum)",
+                             "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 4 * len(W) * args.steps,
+                "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, W, world, rank, dev):
+    import torch
+    import torch.distributed as dist
+
+    steps = max(1, min(args.steps, 3))
+    for s in W:
+        code = s["code"]
+        Fr = s["F"]
+        s["pin_y"] = torch.from_numpy(s["y_host"]).pin_memory()
+        s["pin_known"] = torch.from_numpy(s["x_host"]).pin_memory() if s["known"] is not None else None
+        s["pin_syn"] = s["syn"].cpu().pin_memory()
+        s["pin_out"] = (torch.empty((Fr, code.nb8), dtype=torch.uint8).pin_memory(),
+                        torch.empty(Fr, dtype=torch.int32).pin_memory(),
+                        torch.empty(Fr, dtype=torch.uint8).pin_memory())
+        s["dbuf"] = torch.empty(code.reconcile_device_bytes(Fr), dtype=torch.uint8, device=dev)
+    h2d = sum(s["F"] * (s["code"].nb8 * (2 if s["known"] is not None else 1) + s["code"].mb8) for s in W) * world
+    d2h = sum(s["F"] * (s["code"].nb8 + 5) for s in W) * world
+
+    def one():
+        for s in W:
+            s["code"].reconcile_host(s["w"].qber, s["pin_y"], s["pin_syn"], s["w"].max_iter, True,
+                                     known_bits=s["pin_known"], device_buffer=s["dbuf"], out=s["pin_out"])
+
+    one()   # warm
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = torch.tensor([(time.perf_counter() - t0) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    corrected = 0
+    for s in W:
+        bits, iters, succ = (t.numpy() for t in s["pin_out"])
+        kind = s["w"].pos_kind()
+        diff = bits ^ s["x_host"]
+        if kind is not None:
+            diff &= np.packbits(kind == 0, bitorder="little")[None, :]
+        ok = (succ == 1) & (diff == 0).all(axis=1)
+        corrected += int(ok.sum()) * payload_bits(s["w"])
+    cb = torch.tensor([corrected], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(cb)
+    return {"value": float(cb.item()) / float(dt.item()) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "note": "qkd_reconcile_host per workload: H2D(Bob bits, syndrome) + LLR + decode + D2H(bits, iters, "
+                    "success) on pinned host buffers, host wall clock, max over ranks"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -8,8 +8,12 @@
 
 namespace qkd {
 
+// PTX prmt.b32 in its default mode: selector nibble bit 3 replicates the sign (bit 7) of the
+// selected byte.  (__byte_perm masks the selector to 3 bits and loses that mode.)
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    return __byte_perm(a, b, sel);
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
 }
 __device__ __forceinline__ uint32_t rep4(uint32_t byte) { return byte * 0x01010101u; }
 
