@@ -57,6 +57,20 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def shard(F: int, rank: int, world: int) -> tuple[int, int]:
+    """Global frame ids [a, b) decoded by `rank` (contiguous, even split)."""
+    return rank * F // world, (rank + 1) * F // world
+
+
+def reduce_counters(counters, world: int):
+    """The one collective of the path: SUM all-reduce of the int64 counters."""
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(counters)
+    return counters
+
+
 def payload_bits(w):
     d, p, s = w.rate_adaptive_counts()
     return w.n - p - s
@@ -222,7 +236,7 @@ def run_gpu(args):
     for name in names:
         w = synth.workload(name)
         F = w.frames
-        a, b = rank * F // world, (rank + 1) * F // world
+        a, b = shard(F, rank, world)
         t0 = time.perf_counter()
         x, y, _ = w.gen(a, b - a, nthreads)
         kind = w.pos_kind()
@@ -259,8 +273,7 @@ def run_gpu(args):
             if record:
                 ev[s["name"]].append((e0, e1))
             code.score(s["out"]["bits"], s["x"], s["out"]["success"], counters=counters[i])   # a9
-        if world > 1:
-            dist.all_reduce(counters)                                 # a9: the only collective
+        reduce_counters(counters, world)                              # a9: the only collective
 
     for _ in range(args.warmup):
         step(False)
