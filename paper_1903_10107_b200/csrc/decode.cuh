@@ -1,26 +1,30 @@
-// decode.cuh -- the fused layered decode (check node + variable node + syndrome check +
-// early exit) for one frame group of 4 frames held in byte lanes.
+// decode.cuh -- the fused layered decode (check node + variable node) for one check row of
+// one frame group (4 frames held in the 4 byte lanes of every 32-bit word).
 //
 // Storage forms:
-//   E word   (shared memory, or global for very long frames): byte f = E_j(frame f) + 128
-//   N word   (global workspace, canonical edge order):          byte f = 64 - L_ij(frame f)
-// so that x + 192 = E' + N' (Eq.(8): x = L_ji = E_j' - L_ij^{t-1}) is a plain 16-bit lane add
-// with no overflow (x in [-190, 190]).
+//   E word (shared memory, or global for very long frames): byte f = E_j(frame f) + 127
+//   S word (global workspace):                               byte f = 64 - L_ij(frame f)
+// so that X = x + 191 = E'' + S (Eq.(8): x = L_ji = E_j' - L_ij^{t-1}, exact, in [-190, 190])
+// is a sum of non-negative 16-bit lanes and can be formed on the FMA pipe.
+//
+// Workspace layout: per slot, per block row I, row r owns Dp = roundup4(deg_I) consecutive
+// words (edge k of the row at word k), so a row's messages move with 128-bit loads/stores.
 #pragma once
 #include "swar.cuh"
 
 namespace qkd {
 
 struct DecParams {
-    const int2* layer;        // [Mb] (degree, first base edge)
+    const int4* layer;        // [Mb] (degree, first base edge, L offset in words, Dp)
     const int2* edge;         // [nbase] (J*Z, shift)
     int Mb, Z, nbase, n, m, mb8, nb8;
-    long long n_edges;
+    long long n_edges;        // canonical message count (nbase * Z)
+    long long ws_words;       // workspace words per slot (sum over I of Z * Dp_I)
     const int8_t* llr;        // [F][n]
     const uint8_t* syn;       // [F][mb8]
     long long F, ngroups;
     int T, early_stop, vec_llr;
-    uint32_t* Lws;            // [slots][n_edges]
+    uint32_t* Lws;            // [slots][ws_words]
     uint32_t* Ews;            // [slots][n]   (global-E variant only)
     int* work;                // group work counter
     uint8_t* bits;            // [F][nb8]
@@ -29,107 +33,128 @@ struct DecParams {
     int8_t* fL;               // [F][n_edges] or null
     int8_t* fE;               // [F][n] or null
     unsigned long long* counters;   // [5] or null
-    int TG, GPC, tab_bytes, group_bytes, e_smem;
+    int TG, GPC, slot_bytes, e_bytes, tab_off;
+    Konst K;
 };
 
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// E addressing.  POW2: a = ((r4 + s4) & (4Z - 1)) | cb4, all in bytes, cb4 = slot E base + J*Z*4
+// (slot bases are multiples of 4Z, see make_plan), one IMAD + one LOP3 per edge.  Otherwise
+// words: j = J*Z + (r + s) mod Z.
+template <bool POW2>
+struct Addr {
+    __device__ __forceinline__ static uint32_t at(int2 e, uint32_t r4, uint32_t zm4, int Z, const Konst& K) {
+        if constexpr (POW2) {
+            return (imad(r4, K.one, (uint32_t)e.y) & zm4) | (uint32_t)e.x;
+        } else {
+            int idx = (int)(r4 >> 2) + e.y;
+            idx = idx >= Z ? idx - Z : idx;
+            return (uint32_t)(e.x + idx) << 2;
+        }
+    }
+};
+
 template <bool ESM>
-__device__ __forceinline__ uint32_t ldE(const uint32_t* E, int j) {
-    return E[j];   // shared (ESM) or global; bar.sync orders both for the group
+__device__ __forceinline__ uint32_t ldE(const unsigned char* Eb, uint32_t a) {
+    return *reinterpret_cast<const uint32_t*>(Eb + a);
 }
 template <bool ESM>
-__device__ __forceinline__ void stE(uint32_t* E, int j, uint32_t v) {
-    E[j] = v;
+__device__ __forceinline__ void stE(unsigned char* Eb, uint32_t a, uint32_t v) {
+    *reinterpret_cast<uint32_t*>(Eb + a) = v;
 }
 
-// x192 = x + 192 in two 16x2 words, clamped/packed check input cw = clamp(x,-63,63)+192
+// X = x + 191 in two 16-bit-lane words; cw = clamp(x + 63, 0, 126) packed per frame byte.
 struct EdgeIn {
     uint32_t xlo, xhi, cw;
 };
 
-__device__ __forceinline__ EdgeIn edge_in(uint32_t ew, uint32_t nw) {
+__device__ __forceinline__ EdgeIn edge_in(uint32_t e, uint32_t s, const Konst& K) {
     EdgeIn r;
-    r.xlo = __vadd2(lo16z(ew), lo16z(nw));
-    r.xhi = __vadd2(hi16z(ew), hi16z(nw));
-    const uint32_t clo = __vmins2(__vmaxs2(r.xlo, 0x00810081u), 0x00FF00FFu);
-    const uint32_t chi = __vmins2(__vmaxs2(r.xhi, 0x00810081u), 0x00FF00FFu);
-    r.cw = pack16(clo, chi);          // bytes in [129, 255]; bit 6 = (x >= 0)
-    return r;
+    r.xhi = imad(hi16z(e), K.one, hi16z(s));              // lanes {1,3}: e + s
+    r.xlo = imad(r.xhi, K.m256, imad(e, K.one, s));       // lanes {0,2}: (e + s) - 256 * xhi
+    const uint32_t clo = relu_min(r.xlo, K.b128, 0x007E007Eu);   // clamp(X - 128, 0, 126)
+    const uint32_t chi = relu_min(r.xhi, K.b128, 0x007E007Eu);
+    r.cw = pack16(clo, chi);          // bytes in [0, 126]; bit 6 = (x >= 1) -- x = 0 counts as
+    return r;                         // negative, which is immaterial (R23)
 }
 // check-node magnitude min(|x|, 63) (MSG_max = 63)
-__device__ __forceinline__ uint32_t edge_mag(uint32_t cw) { return __vabsdiffu4(cw, 0xC0C0C0C0u); }
+__device__ __forceinline__ uint32_t edge_mag(uint32_t cw, const Konst& K) { return __vabsdiffu4(cw, K.c63); }
 
 // Given the leave-one-out magnitude o, the sign flag (bit 6 of negf = 1 -> L_new < 0), the
-// edge's x192 words and the pre-layer E word: returns the new N word (stored) and writes
-// the new E word (Algorithm 2 guard on |E'| = E_max, Eq.(9) saturated to +-127).
+// edge's X words and the pre-layer E word: returns the new S word (stored) and writes the new
+// E word (Algorithm 2 guard on |E| = E_max, Eq.(9) saturated to +-127).
 __device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t negf, const EdgeIn& in, uint32_t ew,
-                                             uint32_t& e_out) {
-    const uint32_t M = bmask7(negf << 1);                    // 0xFF where L_new < 0
-    const uint32_t a = o ^ (M & 0x3F3F3F3Fu);                // o or 63-o
-    const uint32_t bp = (M & 0x41414141u) ^ 0xC0C0C0C0u;     // 192 or 129
-    const uint32_t Tp = a + bp;                              // (64 + L_new) + 128
-    const uint32_t Np = 0x01010100u - a - bp;                // 64 - L_new
-    // E' + L_new - L_old clamped: lanes = max(x192 + T - 128, 1) then min 255
-    const uint32_t elo = __vmins2(__viaddmax_s16x2(in.xlo, lo16s(Tp), 0x00010001u), 0x00FF00FFu);
-    const uint32_t ehi = __vmins2(__viaddmax_s16x2(in.xhi, hi16s(Tp), 0x00010001u), 0x00FF00FFu);
-    const uint32_t enew = pack16(elo, ehi);
-    const uint32_t G = bmask7(__vabsdiffu4(ew, 0x80808080u) + 0x01010101u);   // |E| == 127
-    e_out = (G & ew) | (~G & enew);
-    return Np;
+                                             const Konst& K, uint32_t& e_out) {
+    const uint32_t M = bmask7(imad(negf, K.two, 0u));             // 0xFF where L_new < 0
+    const uint32_t om = o & M;
+    const uint32_t Tb = imad(om, K.m2, imad(o, K.one, 0xC0C0C0C0u));   // bytes (64 + L_new) + 128
+    const uint32_t thi = hi16s(Tb);                               // lanes {1,3}: 64 + L_new - 128
+    const uint32_t tlo = imad(imad(thi, K.m256, Tb), K.one, 0xFFFFFF00u);   // lanes {0,2}, same
+    // E + L_new - L_old = x + L_new: lanes relu(min(X + T - 128, 254)) = clamp(.., -127, 127) + 127
+    const uint32_t enew = pack16(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu));
+    const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
+    e_out = lop3<0xCA>(G, ew, enew);                              // G ? ew : enew
+    return imad(Tb, K.m1, 0x01010100u);                           // 128 - T = 64 - L_new
 }
 
+__device__ __forceinline__ uint4 ld4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ void st4(uint32_t* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+__device__ __forceinline__ uint32_t& w4(uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
 // One check row r of a block row with D edges (layered update, Alg. 1/2).
-template <int D, bool ESM>
-__device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, int r, uint32_t* E,
-                                           uint32_t* __restrict__ Lrow, uint32_t nib, bool first) {
-    int addr[D];
+//   et   : the row's D (cb, s) entries;  Lrow : this row's Dp words;  nib : target syndrome bits
+template <int D, bool ESM, bool POW2>
+__device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, uint32_t r4, uint32_t zm4,
+                                           unsigned char* Eb, uint32_t* __restrict__ Lrow, uint32_t nib,
+                                           bool first, const Konst& K) {
+    constexpr int NV = (D + 3) / 4;
+    uint4 S[NV];
+    uint32_t addr[D];
     EdgeIn in[D];
     uint32_t P = 0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-        const int2 e = et[k];
-        int idx = r + e.y;
-        idx = idx >= Z ? idx - Z : idx;
-        addr[k] = e.x + idx;
-    }
+    for (int v = 0; v < NV; ++v) S[v] = first ? make_uint4(0x40404040u, 0x40404040u, 0x40404040u, 0x40404040u)
+                                              : ld4(Lrow + 4 * v);
+#pragma unroll
+    for (int k = 0; k < D; ++k) addr[k] = Addr<POW2>::at(et[k], r4, zm4, Z, K);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        const uint32_t ew = ldE<ESM>(E, addr[k]);
-        const uint32_t nw = first ? 0x40404040u : Lrow[(size_t)k * Z + r];
-        in[k] = edge_in(ew, nw);
+        in[k] = edge_in(ldE<ESM>(Eb, addr[k]), w4(S[k >> 2], k & 3), K);
         P ^= in[k].cw;
     }
     // Eq.(1) with the target bit: L_new of edge k is negative iff
     // s_i ^ XOR_{j != k} [x_j < 0] = s_i ^ ((D-1)&1) ^ P ^ nonneg_k   (bit 6)
     const uint32_t Q = P ^ nib_to_bit6(nib) ^ (((D - 1) & 1) ? 0x40404040u : 0u);
     // emit edge k as soon as its leave-one-out magnitude is known (keeps the live set small)
+    // edges are emitted from k = D-1 down to 0, so a 128-bit group of new messages is complete
+    // (and stored) once its lowest edge is done
     auto emit = [&](int k, uint32_t o) {
-        const uint32_t ew = ldE<ESM>(E, addr[k]);
+        const uint32_t ew = ldE<ESM>(Eb, addr[k]);
         uint32_t eo;
-        const uint32_t np = edge_out(o, Q ^ in[k].cw, in[k], ew, eo);
-        stE<ESM>(E, addr[k], eo);
-        Lrow[(size_t)k * Z + r] = np;
+        w4(S[k >> 2], k & 3) = edge_out(o, Q ^ in[k].cw, in[k], ew, K, eo);
+        stE<ESM>(Eb, addr[k], eo);
+        if ((k & 3) == 0) st4(Lrow + k, S[k >> 2]);
     };
     if constexpr (D == 1) {
         emit(0, 0x3F3F3F3Fu);                       // empty box-plus -> MSG_max (R6)
     } else if constexpr (D == 2) {
-        emit(0, edge_mag(in[1].cw));
-        emit(1, edge_mag(in[0].cw));
+        emit(1, edge_mag(in[0].cw, K));
+        emit(0, edge_mag(in[1].cw, K));
     } else {
         // forward/backward leave-one-out in ascending block column (R6)
         uint32_t F[D - 1];
-        F[0] = edge_mag(in[0].cw);
+        F[0] = edge_mag(in[0].cw, K);
 #pragma unroll
-        for (int k = 1; k <= D - 2; ++k) F[k] = tau4(F[k - 1], edge_mag(in[k].cw));
+        for (int k = 1; k <= D - 2; ++k) F[k] = tau4(F[k - 1], edge_mag(in[k].cw, K), K);
         emit(D - 1, F[D - 2]);
-        uint32_t B = edge_mag(in[D - 1].cw);
+        uint32_t B = edge_mag(in[D - 1].cw, K);
 #pragma unroll
         for (int k = D - 2; k >= 1; --k) {
-            emit(k, tau4(F[k - 1], B));
-            B = tau4(edge_mag(in[k].cw), B);
+            emit(k, tau4(F[k - 1], B, K));
+            B = tau4(edge_mag(in[k].cw, K), B, K);
         }
         emit(0, B);
     }
@@ -137,46 +162,40 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, i
 
 // Runtime-degree variant (any degree <= 64), same arithmetic; state in local memory.
 template <bool ESM>
-__device__ __noinline__ void row_update_generic(const int2* __restrict__ et, int D, int Z, int r,
-                                                uint32_t* E, uint32_t* __restrict__ Lrow, uint32_t nib,
-                                                bool first) {
-    int addr[64];
+__device__ __noinline__ void row_update_generic(const int2* __restrict__ et, int D, int Z, uint32_t r4,
+                                                unsigned char* Eb, uint32_t* __restrict__ Lrow, uint32_t nib,
+                                                bool first, const Konst K) {
+    uint32_t addr[64], S[64], F[64], o[64];
     EdgeIn in[64];
-    uint32_t F[64], o[64];
     uint32_t P = 0;
     for (int k = 0; k < D; ++k) {
-        const int2 e = et[k];
-        int idx = r + e.y;
-        idx = idx >= Z ? idx - Z : idx;
-        addr[k] = e.x + idx;
-        const uint32_t ew = ldE<ESM>(E, addr[k]);
-        const uint32_t nw = first ? 0x40404040u : Lrow[(size_t)k * Z + r];
-        in[k] = edge_in(ew, nw);
+        addr[k] = Addr<false>::at(et[k], r4, 0u, Z, K);
+        S[k] = first ? 0x40404040u : Lrow[k];
+        in[k] = edge_in(ldE<ESM>(Eb, addr[k]), S[k], K);
         P ^= in[k].cw;
     }
     const uint32_t Q = P ^ nib_to_bit6(nib) ^ (((D - 1) & 1) ? 0x40404040u : 0u);
     if (D == 1) {
         o[0] = 0x3F3F3F3Fu;
     } else if (D == 2) {
-        o[0] = edge_mag(in[1].cw);
-        o[1] = edge_mag(in[0].cw);
+        o[0] = edge_mag(in[1].cw, K);
+        o[1] = edge_mag(in[0].cw, K);
     } else {
-        F[0] = edge_mag(in[0].cw);
-        for (int k = 1; k <= D - 2; ++k) F[k] = tau4(F[k - 1], edge_mag(in[k].cw));
-        uint32_t B = edge_mag(in[D - 1].cw);
+        F[0] = edge_mag(in[0].cw, K);
+        for (int k = 1; k <= D - 2; ++k) F[k] = tau4(F[k - 1], edge_mag(in[k].cw, K), K);
+        uint32_t B = edge_mag(in[D - 1].cw, K);
         o[D - 1] = F[D - 2];
         for (int k = D - 2; k >= 1; --k) {
-            o[k] = tau4(F[k - 1], B);
-            B = tau4(edge_mag(in[k].cw), B);
+            o[k] = tau4(F[k - 1], B, K);
+            B = tau4(edge_mag(in[k].cw, K), B, K);
         }
         o[0] = B;
     }
     for (int k = 0; k < D; ++k) {
-        const uint32_t ew = ldE<ESM>(E, addr[k]);
+        const uint32_t ew = ldE<ESM>(Eb, addr[k]);
         uint32_t eo;
-        const uint32_t np = edge_out(o[k], Q ^ in[k].cw, in[k], ew, eo);
-        stE<ESM>(E, addr[k], eo);
-        Lrow[(size_t)k * Z + r] = np;
+        Lrow[k] = edge_out(o[k], Q ^ in[k].cw, in[k], ew, K, eo);
+        stE<ESM>(Eb, addr[k], eo);
     }
 }
 

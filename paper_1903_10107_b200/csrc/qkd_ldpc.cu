@@ -39,9 +39,10 @@ struct qkd_code {
     int32_t Mb = 0, Nb = 0, Z = 0;
     int64_t n = 0, m = 0, n_edges = 0;
     int32_t nbase = 0, maxdeg = 0;
-    std::vector<int2> layer;   // (deg, first base edge)
+    std::vector<int4> layer;   // (deg, first base edge, workspace word offset of the block row, Dp)
+    int64_t ws_words = 0;      // workspace words per slot: sum_I Z * roundup4(deg_I)
     std::vector<int2> edge;    // (J*Z, shift)
-    int2* d_layer = nullptr;
+    int4* d_layer = nullptr;
     int2* d_edge = nullptr;
     uint8_t* d_kind = nullptr;     // pos kind or null
     uint8_t* d_payload = nullptr;  // packed payload mask or null (= all payload)
@@ -57,17 +58,20 @@ namespace {
 
 constexpr int kFramesPerGroup = 4;
 
-template <int DMAX, bool ESM>
-__device__ __forceinline__ void layer_pass(const DecParams& p, int d, const int2* et, int t, uint32_t* E,
-                                           uint32_t* Lrow, const uint8_t* synI, bool first) {
+template <int DMAX, bool ESM, bool POW2>
+__device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, const int2* et, int t,
+                                           unsigned char* Eb, uint32_t* Lslot, const uint8_t* synI, bool first,
+                                           const Konst& K) {
+    const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
     if constexpr (DMAX > 0) {
-        switch (d) {
-#define QKD_CASE(DD)                                                                      \
-    case DD:                                                                              \
-        if constexpr (DD <= DMAX) {                                                       \
-            for (int r = t; r < p.Z; r += p.TG) row_update<DD, ESM>(et, p.Z, r, E, Lrow, synI[r], first); \
-            return;                                                                       \
-        }                                                                                 \
+        switch (li.x) {
+#define QKD_CASE(DD)                                                                                     \
+    case DD:                                                                                             \
+        if constexpr (DD <= DMAX) {                                                                      \
+            for (int r = t; r < p.Z; r += p.TG)                                                          \
+                row_update<DD, ESM, POW2>(et, p.Z, 4u * r, zm4, Eb, Lslot + li.z + r * li.w, synI[r], first, K); \
+            return;                                                                                      \
+        }                                                                                                \
         break;
             QKD_CASE(1) QKD_CASE(2) QKD_CASE(3) QKD_CASE(4) QKD_CASE(5) QKD_CASE(6) QKD_CASE(7)
             QKD_CASE(8) QKD_CASE(9) QKD_CASE(10) QKD_CASE(11) QKD_CASE(12) QKD_CASE(13)
@@ -79,29 +83,27 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, int d, const int2
         }
         __trap();   // the host never selects a DMAX kernel for a code with a larger degree
     } else {
-        for (int r = t; r < p.Z; r += p.TG) row_update_generic<ESM>(et, d, p.Z, r, E, Lrow, synI[r], first);
+        for (int r = t; r < p.Z; r += p.TG)
+            row_update_generic<ESM>(et, li.x, p.Z, 4u * r, Eb, Lslot + li.z + r * li.w, synI[r], first, K);
     }
 }
 
 // per-lane syndrome violation mask (bit f set = frame f violates some parity check),
-// group-uniform.  Hard decision bit = (E < 0) = NOT bit 7 of E' (R9).
-template <bool ESM>
-__device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int2* s_layer, const int2* s_edge,
-                                                  const uint32_t* E, const uint8_t* sSyn, int t,
-                                                  uint32_t* flags, int& chk, int bar) {
+// group-uniform.  Hard decision bit = (E < 0) = NOT bit 7 of (E'' + 1), E'' = E + 127 (R9).
+template <bool ESM, bool POW2>
+__device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int4* s_layer, const int2* s_edge,
+                                                  const unsigned char* Eb, const uint8_t* sSyn, int t,
+                                                  uint32_t* flags, int& chk, int bar, const Konst& K) {
+    const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
     uint32_t v = 0;
     for (int I = 0; I < p.Mb; ++I) {
-        const int2 li = s_layer[I];
+        const int4 li = s_layer[I];
         const int2* et = s_edge + li.y;
         const uint32_t par = (li.x & 1) ? 0x80808080u : 0u;
         for (int r = t; r < p.Z; r += p.TG) {
             uint32_t acc = nib_to_bit7(sSyn[I * p.Z + r]) ^ par;
-            for (int k = 0; k < li.x; ++k) {
-                const int2 e = et[k];
-                int idx = r + e.y;
-                idx = idx >= p.Z ? idx - p.Z : idx;
-                acc ^= ldE<ESM>(E, e.x + idx);
-            }
+            for (int k = 0; k < li.x; ++k)
+                acc ^= imad(ldE<ESM>(Eb, Addr<POW2>::at(et[k], 4u * r, zm4, p.Z, K)), K.one, 0x01010101u);
             v |= acc;
         }
     }
@@ -116,9 +118,8 @@ __device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int2
 }
 
 // write the outputs of the lanes in `mask` (state at their stopping iteration)
-template <bool ESM>
-__device__ void finalize(const DecParams& p, const uint32_t* E, const uint32_t* Lg, long long f0, uint32_t mask,
-                         int it, uint32_t succ_mask, bool first, int t) {
+__device__ void finalize(const DecParams& p, const int4* s_layer, const uint32_t* Eslot, const uint32_t* Lslot,
+                         long long f0, uint32_t mask, int it, uint32_t succ_mask, bool first, int t) {
     const int lane = threadIdx.x & 31;
     for (int f = 0; f < kFramesPerGroup; ++f) {
         if (!((mask >> f) & 1u)) continue;
@@ -126,19 +127,27 @@ __device__ void finalize(const DecParams& p, const uint32_t* E, const uint32_t* 
         uint8_t* brow = p.bits + frame * p.nb8;
         for (int jw = t & ~31; jw < p.n; jw += p.TG) {
             const int j = jw + lane;
-            const bool b = j < p.n && !((ldE<ESM>(E, j < p.n ? j : 0) >> (8 * f + 7)) & 1u);
+            const bool b = j < p.n && !(((Eslot[j < p.n ? j : 0] + 0x01010101u) >> (8 * f + 7)) & 1u);
             const uint32_t bal = __ballot_sync(0xffffffffu, b);
             const int byte = (jw >> 3) + lane;
             if (lane < 4 && byte < p.nb8) brow[byte] = (uint8_t)(bal >> (8 * lane));
         }
         if (p.fE) {
             int8_t* erow = p.fE + frame * p.n;
-            for (int j = t; j < p.n; j += p.TG) erow[j] = (int8_t)(((ldE<ESM>(E, j) >> (8 * f)) & 0xFFu) ^ 0x80u);
+            for (int j = t; j < p.n; j += p.TG) erow[j] = (int8_t)((int)((Eslot[j] >> (8 * f)) & 0xFFu) - 127);
         }
         if (p.fL) {
             int8_t* lrow = p.fL + frame * p.n_edges;
-            for (long long e = t; e < p.n_edges; e += p.TG)
-                lrow[e] = first ? (int8_t)0 : (int8_t)(64 - (int)((Lg[e] >> (8 * f)) & 0xFFu));
+            for (int I = 0; I < p.Mb; ++I) {
+                const int4 li = s_layer[I];
+                const int cnt = li.x * p.Z;
+                for (int q = t; q < cnt; q += p.TG) {
+                    const int k = q / p.Z, r = q - k * p.Z;
+                    const long long e = (long long)(li.y + k) * p.Z + r;     // canonical edge order
+                    lrow[e] = first ? (int8_t)0
+                                    : (int8_t)(64 - (int)((Lslot[li.z + r * li.w + k] >> (8 * f)) & 0xFFu));
+                }
+            }
         }
         if (t == 0) {
             const int s = (succ_mask >> f) & 1;
@@ -153,26 +162,34 @@ __device__ void finalize(const DecParams& p, const uint32_t* E, const uint32_t* 
     }
 }
 
-template <int DMAX, bool ESM>
+template <int DMAX, bool ESM, bool POW2>
 __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1)
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    int2* s_layer = reinterpret_cast<int2*>(smem);
-    int2* s_edge = s_layer + p.Mb;
+    const Konst K = p.K.in_regs();
+    // tables: layer info, then one edge table per slot with the slot's E base folded in
+    int4* s_layer = reinterpret_cast<int4*>(smem + p.tab_off);
+    int2* s_edges = reinterpret_cast<int2*>(s_layer + p.Mb);
     for (int i = threadIdx.x; i < p.Mb; i += blockDim.x) s_layer[i] = p.layer[i];
-    for (int i = threadIdx.x; i < p.nbase; i += blockDim.x) s_edge[i] = p.edge[i];
+    for (int i = threadIdx.x; i < p.GPC * p.nbase; i += blockDim.x) {
+        const int sl = i / p.nbase;
+        const int2 e = p.edge[i - sl * p.nbase];
+        s_edges[i] = POW2 ? make_int2(sl * p.slot_bytes + 4 * e.x, 4 * e.y) : e;
+    }
     __syncthreads();
 
     const int slot = threadIdx.x / p.TG;
     const int t = threadIdx.x - slot * p.TG;
     const int bar = 1 + slot;
-    unsigned char* gbase = smem + p.tab_bytes + (size_t)slot * p.group_bytes;
+    const int2* s_edge = s_edges + slot * p.nbase;
+    unsigned char* sbase = smem + (size_t)slot * p.slot_bytes;
     const long long gslot = (long long)blockIdx.x * p.GPC + slot;
-    uint32_t* E = ESM ? reinterpret_cast<uint32_t*>(gbase) : p.Ews + gslot * (long long)p.n;
-    uint8_t* sSyn = gbase + p.e_smem;
+    uint32_t* Eslot = ESM ? reinterpret_cast<uint32_t*>(sbase) : p.Ews + gslot * (long long)p.n;
+    unsigned char* Eb = ESM ? (POW2 ? smem : sbase) : reinterpret_cast<unsigned char*>(Eslot);
+    uint8_t* sSyn = sbase + p.e_bytes;
     int* ctl = reinterpret_cast<int*>(sSyn + ((p.m + 15) & ~15));   // [0] group id, [1..2] flags
     uint32_t* flags = reinterpret_cast<uint32_t*>(ctl + 1);
-    uint32_t* Lg = p.Lws + gslot * p.n_edges;
+    uint32_t* Lslot = p.Lws + gslot * p.ws_words;
 
     for (;;) {
         if (t == 0) ctl[0] = atomicAdd(p.work, 1);
@@ -182,7 +199,7 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
         const long long f0 = g * kFramesPerGroup;
         const int nl = (int)min((long long)kFramesPerGroup, p.F - f0);
 
-        // ---- E <- channel LLR, frame-interleaved, offset +128
+        // ---- E <- channel LLR, frame-interleaved, stored as E + 127 = (llr ^ 0x80) - 1
         if (p.vec_llr) {
             const int n4 = p.n >> 2;
             for (int q = t; q < n4; q += p.TG) {
@@ -190,12 +207,12 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
 #pragma unroll
                 for (int f = 0; f < 4; ++f)
                     r[f] = f < nl ? __ldcs(reinterpret_cast<const uint32_t*>(p.llr + (f0 + f) * p.n) + q) : 0x7F7F7F7Fu;
-                const uint32_t a = prmt(r[0], r[1], 0x5140u), b = prmt(r[2], r[3], 0x5140u);
-                const uint32_t c = prmt(r[0], r[1], 0x7362u), d = prmt(r[2], r[3], 0x7362u);
-                stE<ESM>(E, 4 * q + 0, prmt(a, b, 0x5410u) ^ 0x80808080u);
-                stE<ESM>(E, 4 * q + 1, prmt(a, b, 0x7632u) ^ 0x80808080u);
-                stE<ESM>(E, 4 * q + 2, prmt(c, d, 0x5410u) ^ 0x80808080u);
-                stE<ESM>(E, 4 * q + 3, prmt(c, d, 0x7632u) ^ 0x80808080u);
+                const uint32_t a = prmt<0x5140u>(r[0], r[1]), b = prmt<0x5140u>(r[2], r[3]);
+                const uint32_t c = prmt<0x7362u>(r[0], r[1]), d = prmt<0x7362u>(r[2], r[3]);
+                Eslot[4 * q + 0] = (prmt<0x5410u>(a, b) ^ 0x80808080u) - 0x01010101u;
+                Eslot[4 * q + 1] = (prmt<0x7632u>(a, b) ^ 0x80808080u) - 0x01010101u;
+                Eslot[4 * q + 2] = (prmt<0x5410u>(c, d) ^ 0x80808080u) - 0x01010101u;
+                Eslot[4 * q + 3] = (prmt<0x7632u>(c, d) ^ 0x80808080u) - 0x01010101u;
             }
         } else {
             for (int j = t; j < p.n; j += p.TG) {
@@ -203,9 +220,9 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
 #pragma unroll
                 for (int f = 0; f < 4; ++f) {
                     const uint32_t v = f < nl ? (uint8_t)p.llr[(f0 + f) * p.n + j] : 0x7Fu;
-                    w |= (v ^ 0x80u) << (8 * f);
+                    w |= ((v ^ 0x80u) - 1u) << (8 * f);
                 }
-                stE<ESM>(E, j, w);
+                Eslot[j] = w;
             }
         }
         // ---- target syndrome: one nibble per check row (bit f = frame f)
@@ -230,10 +247,10 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
         uint32_t active = (1u << nl) - 1u;
         int chk = 0;
         if (p.early_stop) {   // iteration-0 check (R10)
-            const uint32_t viol = syndrome_viol<ESM>(p, s_layer, s_edge, E, sSyn, t, flags, chk, bar);
+            const uint32_t viol = syndrome_viol<ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
             const uint32_t done = active & ~viol;
             if (done) {
-                finalize<ESM>(p, E, Lg, f0, done, 0, done, true, t);
+                finalize(p, s_layer, Eslot, Lslot, f0, done, 0, done, true, t);
                 group_bar(bar, p.TG);
             }
             active &= viol;
@@ -243,16 +260,15 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
             ++it;
             const bool first = it == 1;
             for (int I = 0; I < p.Mb; ++I) {
-                const int2 li = s_layer[I];
-                layer_pass<DMAX, ESM>(p, li.x, s_edge + li.y, t, E, Lg + (long long)li.y * p.Z, sSyn + I * p.Z,
-                                      first);
+                const int4 li = s_layer[I];
+                layer_pass<DMAX, ESM, POW2>(p, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z, first, K);
                 group_bar(bar, p.TG);
             }
             if (p.early_stop) {
-                const uint32_t viol = syndrome_viol<ESM>(p, s_layer, s_edge, E, sSyn, t, flags, chk, bar);
+                const uint32_t viol = syndrome_viol<ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
                 const uint32_t done = active & ~viol;
                 if (done) {
-                    finalize<ESM>(p, E, Lg, f0, done, it, done, false, t);
+                    finalize(p, s_layer, Eslot, Lslot, f0, done, it, done, false, t);
                     group_bar(bar, p.TG);
                 }
                 active &= viol;
@@ -260,8 +276,9 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
         }
         if (active) {   // ran out of iterations (or early_stop = 0): state after sweep T (R12)
             uint32_t succ = 0;
-            if (!p.early_stop) succ = active & ~syndrome_viol<ESM>(p, s_layer, s_edge, E, sSyn, t, flags, chk, bar);
-            finalize<ESM>(p, E, Lg, f0, active, it, succ, it == 0, t);
+            if (!p.early_stop)
+                succ = active & ~syndrome_viol<ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
+            finalize(p, s_layer, Eslot, Lslot, f0, active, it, succ, it == 0, t);
         }
         group_bar(bar, p.TG);
     }
@@ -270,7 +287,7 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
 // --------------------------------------------------------------------------------------
 // Alice's syndrome: one CTA per frame, frame bits staged in shared memory.
 // --------------------------------------------------------------------------------------
-__global__ void syndrome_kernel(const int2* __restrict__ layer, const int2* __restrict__ edge, int Mb, int Z,
+__global__ void syndrome_kernel(const int4* __restrict__ layer, const int2* __restrict__ edge, int Mb, int Z,
                                 int n, int m, int nb8, int mb8, long long F, const uint8_t* __restrict__ bits,
                                 uint8_t* __restrict__ syn) {
     extern __shared__ __align__(16) unsigned char sb[];
@@ -284,7 +301,7 @@ __global__ void syndrome_kernel(const int2* __restrict__ layer, const int2* __re
             uint32_t par = 0;
             if (i < m) {
                 const int I = i / Z, r = i - I * Z;
-                const int2 li = layer[I];
+                const int4 li = layer[I];
                 for (int k = 0; k < li.x; ++k) {
                     const int2 e = edge[li.y + k];
                     int idx = r + e.y;
@@ -359,13 +376,13 @@ __global__ void score_kernel(int nb8, long long F, const uint8_t* __restrict__ b
     }
 }
 
-__global__ void tau_table_kernel(uint8_t* out) {
+__global__ void tau_table_kernel(uint8_t* out, Konst K) {
     const int p = threadIdx.x;   // 64 threads
     for (int w = 0; w < 16; ++w) {
         const uint32_t a = rep4((uint32_t)p);
         const uint32_t b = (uint32_t)(4 * w) | ((uint32_t)(4 * w + 1) << 8) | ((uint32_t)(4 * w + 2) << 16) |
                            ((uint32_t)(4 * w + 3) << 24);
-        const uint32_t t = tau4(a, b);
+        const uint32_t t = tau4(a, b, K);
         for (int q = 0; q < 4; ++q) out[p * 64 + 4 * w + q] = (uint8_t)(t >> (8 * q));
     }
 }
@@ -374,8 +391,9 @@ __global__ void tau_table_kernel(uint8_t* out) {
 // launch planning
 // --------------------------------------------------------------------------------------
 struct Plan {
-    int variant = 0;   // 1: DMAX 8 smem, 2: DMAX 20 smem, 3: generic smem, 4: generic global E
-    int TG = 0, GPC = 0, grid = 0, smem = 0, tab_bytes = 0, group_bytes = 0, e_smem = 0;
+    int variant = 0;   // 1: degree <= 8 smem E, 2: degree <= 20 smem E, 3: generic smem E, 4: generic global E
+    bool pow2 = false; // Z a power of two (byte-OR circulant addressing)
+    int TG = 0, GPC = 0, grid = 0, smem = 0, slot_bytes = 0, e_bytes = 0, tab_off = 0;
     long long ngroups = 0, slots = 0;
     size_t ws_L = 0, ws_E = 0, ws_total = 0;
 };
@@ -398,19 +416,22 @@ DevInfo dev_info(int dev) {
     return cache[dev];
 }
 
-template <int DMAX, bool ESM>
+template <int DMAX, bool ESM, bool POW2>
 const void* kfun() {
-    return reinterpret_cast<const void*>(&decode_kernel<DMAX, ESM>);
+    return reinterpret_cast<const void*>(&decode_kernel<DMAX, ESM, POW2>);
 }
 
-const void* kernel_of(int variant) {
+const void* kernel_of(int variant, bool pow2) {
     switch (variant) {
-        case 1: return kfun<8, true>();
-        case 2: return kfun<20, true>();
-        case 3: return kfun<0, true>();
-        default: return kfun<0, false>();
+        case 1: return pow2 ? kfun<8, true, true>() : kfun<8, true, false>();
+        case 2: return pow2 ? kfun<20, true, true>() : kfun<20, true, false>();
+        case 3: return kfun<0, true, false>();
+        default: return kfun<0, false, false>();
     }
 }
+
+// 1, 2, -1, -2, -256 as kernel arguments: opaque to ptxas, so a*one + c stays an IMAD (FMA pipe)
+Konst runtime_konst() { return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu}; }
 
 int make_plan(const qkd_code* c, long long F, Plan& pl) {
     int dev = 0;
@@ -418,27 +439,35 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     DevInfo di = dev_info(dev);
     if (!di.ok) return fail(QKD_ECUDA, "cannot query device attributes");
     pl.ngroups = (F + kFramesPerGroup - 1) / kFramesPerGroup;
-    pl.tab_bytes = (int)(((size_t)(c->Mb + c->nbase) * sizeof(int2) + 15) & ~size_t(15));
-    const int syn_bytes = (int)((c->m + 15) & ~15LL) + 16;
+    const long long syn_ctl = ((c->m + 15) & ~15LL) + 16;
     const long long e_bytes = 4LL * c->n;
-    const bool fits = pl.tab_bytes + e_bytes + syn_bytes <= di.smem_optin;
+    const long long tab1 = (long long)c->Mb * sizeof(int4) + (long long)c->nbase * sizeof(int2);
+    const bool fits = e_bytes + syn_ctl + tab1 <= di.smem_optin;
     if (fits && c->maxdeg <= 8) pl.variant = 1;
     else if (fits && c->maxdeg <= 20) pl.variant = 2;
     else if (fits) pl.variant = 3;
     else pl.variant = 4;
+    pl.pow2 = (pl.variant <= 2) && ((c->Z & (c->Z - 1)) == 0);
     const int tg_max = pl.variant == 1 ? 1024 : (pl.variant == 2 ? 512 : 256);
     pl.TG = (int)std::min<long long>(((long long)c->Z + 31) / 32 * 32, tg_max);
-    pl.e_smem = pl.variant == 4 ? 0 : (int)e_bytes;
-    pl.group_bytes = pl.e_smem + syn_bytes;
-    if (pl.tab_bytes + pl.group_bytes > di.smem_optin)
-        return fail(QKD_EUNSUP, "frame too long for the shared-memory syndrome buffer");
+    pl.e_bytes = pl.variant == 4 ? 0 : (int)e_bytes;
+    long long slot = (pl.e_bytes + syn_ctl + 15) & ~15LL;   // 16-byte aligned slots and tables
+    if (pl.pow2) {   // slot E bases must be multiples of 4Z for the byte-OR addressing
+        const long long al = 4LL * c->Z;
+        slot = (slot + al - 1) / al * al;
+    }
+    pl.slot_bytes = (int)slot;
+    if (slot + tab1 > di.smem_optin) return fail(QKD_EUNSUP, "frame too long for the shared-memory buffers");
     int gpc = std::min(15, tg_max / pl.TG);
-    gpc = std::min<int>(gpc, (di.smem_optin - pl.tab_bytes) / pl.group_bytes);
+    while (gpc > 1 && (long long)gpc * (slot + (long long)c->nbase * sizeof(int2)) + c->Mb * sizeof(int4) >
+                          (long long)di.smem_optin)
+        --gpc;
     const long long need = (pl.ngroups + di.sms - 1) / di.sms;
     gpc = (int)std::max<long long>(1, std::min<long long>(gpc, need));
     pl.GPC = gpc;
-    pl.smem = pl.tab_bytes + gpc * pl.group_bytes;
-    const void* k = kernel_of(pl.variant);
+    pl.tab_off = gpc * pl.slot_bytes;
+    pl.smem = pl.tab_off + (int)(c->Mb * sizeof(int4) + (size_t)gpc * c->nbase * sizeof(int2));
+    const void* k = kernel_of(pl.variant, pl.pow2);
     QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
     int per_sm = 0;
     QKD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.TG * pl.GPC, pl.smem));
@@ -446,7 +475,7 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     const long long ctas = (pl.ngroups + gpc - 1) / gpc;
     pl.grid = (int)std::max<long long>(1, std::min<long long>(ctas, (long long)per_sm * di.sms));
     pl.slots = (long long)pl.grid * gpc;
-    pl.ws_L = (size_t)pl.slots * (size_t)c->n_edges * 4;
+    pl.ws_L = (size_t)pl.slots * (size_t)c->ws_words * 4;
     pl.ws_E = pl.variant == 4 ? (size_t)pl.slots * (size_t)c->n * 4 : 0;
     pl.ws_total = 256 + pl.ws_L + pl.ws_E;
     return QKD_OK;
@@ -474,7 +503,7 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
     c->n = (int64_t)Nb * Z;
     c->m = (int64_t)Mb * Z;
     for (int I = 0; I < Mb; ++I) {
-        int2 li = make_int2(0, (int)c->edge.size());
+        int4 li = make_int4(0, (int)c->edge.size(), 0, 0);
         for (int J = 0; J < Nb; ++J) {
             const int s = base_shifts[(size_t)I * Nb + J];
             if (s < -1 || s >= Z) {
@@ -492,14 +521,21 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
             return fail(QKD_EUNSUP, "check degree > 64 in block row " + std::to_string(I));
         }
         c->maxdeg = std::max(c->maxdeg, li.x);
+        li.w = (li.x + 3) & ~3;
+        li.z = (int)c->ws_words;
+        c->ws_words += (int64_t)Z * li.w;
+        if (c->ws_words > (1LL << 31) - 1) {
+            delete c;
+            return fail(QKD_EUNSUP, "code too large for the 32-bit workspace offsets");
+        }
         c->layer.push_back(li);
     }
     c->nbase = (int)c->edge.size();
     c->n_edges = (int64_t)c->nbase * Z;
     cudaError_t e = cudaGetDevice(&c->device);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_layer, sizeof(int2) * c->layer.size());
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_layer, sizeof(int4) * c->layer.size());
     if (e == cudaSuccess) e = cudaMalloc(&c->d_edge, sizeof(int2) * std::max<size_t>(1, c->edge.size()));
-    if (e == cudaSuccess) e = cudaMemcpy(c->d_layer, c->layer.data(), sizeof(int2) * c->layer.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_layer, c->layer.data(), sizeof(int4) * c->layer.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !c->edge.empty())
         e = cudaMemcpy(c->d_edge, c->edge.data(), sizeof(int2) * c->edge.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && pos_kind) {
@@ -599,7 +635,7 @@ int qkd_launch_info(const qkd_code* c, int64_t F, int32_t* info) {
     Plan pl;
     const int rc = make_plan(c, F, pl);
     if (rc) return rc;
-    info[0] = pl.variant;
+    info[0] = pl.variant + (pl.pow2 ? 10 : 0);
     info[1] = pl.TG;
     info[2] = pl.GPC;
     info[3] = pl.grid;
@@ -632,6 +668,7 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
     p.mb8 = (int)((c->m + 7) / 8);
     p.nb8 = (int)((c->n + 7) / 8);
     p.n_edges = c->n_edges;
+    p.ws_words = c->ws_words;
     p.llr = llr;
     p.syn = syn;
     p.F = F;
@@ -650,18 +687,15 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
     p.counters = reinterpret_cast<unsigned long long*>(counters);
     p.TG = pl.TG;
     p.GPC = pl.GPC;
-    p.tab_bytes = pl.tab_bytes;
-    p.group_bytes = pl.group_bytes;
-    p.e_smem = pl.e_smem;
+    p.slot_bytes = pl.slot_bytes;
+    p.e_bytes = pl.e_bytes;
+    p.tab_off = pl.tab_off;
+    p.K = runtime_konst();
     cudaStream_t st = (cudaStream_t)stream;
     QKD_CK(cudaMemsetAsync(p.work, 0, sizeof(int), st));
     const dim3 grid(pl.grid), block(pl.TG * pl.GPC);
-    switch (pl.variant) {
-        case 1: decode_kernel<8, true><<<grid, block, pl.smem, st>>>(p); break;
-        case 2: decode_kernel<20, true><<<grid, block, pl.smem, st>>>(p); break;
-        case 3: decode_kernel<0, true><<<grid, block, pl.smem, st>>>(p); break;
-        default: decode_kernel<0, false><<<grid, block, pl.smem, st>>>(p); break;
-    }
+    void* args[] = {&p};
+    QKD_CK(cudaLaunchKernel(kernel_of(pl.variant, pl.pow2), grid, block, args, pl.smem, st));
     QKD_CK(cudaGetLastError());
     return QKD_OK;
 }
@@ -732,7 +766,7 @@ int qkd_reconcile_host(const qkd_code* c, double qber, int64_t F, const uint8_t*
 
 int qkd_tau_table(uint8_t* out, void* stream) {
     if (!out) return fail(QKD_EINVAL, "null buffer");
-    tau_table_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(out);
+    tau_table_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(out, runtime_konst());
     QKD_CK(cudaGetLastError());
     return QKD_OK;
 }

@@ -1,52 +1,97 @@
-// swar.cuh -- packed 4-frame (u8x4) and 2-frame (s16x2) integer arithmetic for the
-// sm_100a decode kernels.  Each 32-bit word holds one int8 quantity for 4 independent
-// frames (frame f in byte f).  Only ops that are native on sm_100a are used on the hot
-// path: VABSDIFF4.U8, VIADD.16x2, VIMNMX.S16x2, VIADDMNMX.S16x2 (DPX), PRMT, LOP3, IADD3,
-// SHF (see DESIGN.md §5 "instruction budget").
+// swar.cuh -- packed 4-frame (u8x4) and 2-frame (16x2) integer arithmetic for the sm_100a
+// decode kernels.  Each 32-bit word holds one int8 quantity for 4 independent frames (frame f
+// in byte f).  Only ops that are native on sm_100a are used:
+//   ALU pipe: LOP3, SHF, PRMT, VABSDIFF4.U8, VIMNMX/VIADDMNMX(.RELU).S16x2
+//   FMA pipe: IMAD, VIADD.16x2
+// Both pipes issue one warp instruction every 2 cycles per SM sub-partition (measured with
+// tools/pipe_probe.cu), so the arithmetic below is written to split evenly between them: adds
+// of constants, shifts-left, negations and 16-bit lane unpacking go through IMAD with an opaque
+// runtime multiplier (Konst), which ptxas cannot fold back into an ALU-pipe IADD3.
 #pragma once
 #include <cstdint>
 
 namespace qkd {
 
+// runtime constants 1, 2, -1, -2, -256, the lane bias -128|-128 and the byte constants
+// 0x3F3F3F3F / 0x7F7F7F7F (kernel parameters, opaque
+// to the compiler); in_regs() pins them in ordinary registers so ptxas neither folds them nor
+// re-materialises them per use.
+struct Konst {
+    uint32_t one, two, m1, m2, m256, b128, c63, c127;
+    __device__ __forceinline__ Konst in_regs() const {
+        Konst k;
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.one) : "r"(one));
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.two) : "r"(two));
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.m1) : "r"(m1));
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.m2) : "r"(m2));
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.m256) : "r"(m256));
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.b128) : "r"(b128));
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.c63) : "r"(c63));
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.c127) : "r"(c127));
+        return k;
+    }
+};
+
 // PTX prmt.b32 in its default mode: selector nibble bit 3 replicates the sign (bit 7) of the
 // selected byte.  (__byte_perm masks the selector to 3 bits and loses that mode.)
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+template <uint32_t SEL>
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b) {
     uint32_t r;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "n"(SEL));
     return r;
 }
 __device__ __forceinline__ uint32_t rep4(uint32_t byte) { return byte * 0x01010101u; }
 
-// Algorithm 1 (P:119-132) on 4 byte lanes, inputs already clamped to [0, 63].
-//   d = |a-b|, l = min(a,b) = (a+b-d)/2
-//   tau = l - c,  c = [l>=3]([d<2]+[d<6]) + [1<=l<=2][d<4]      (l = 0 -> 0)
-// The comparisons are read from bit 7 of (v + (128-k)), which never carries across a byte
-// because v <= 63.  tau >= 0 in every lane, so the final subtraction never borrows.
-__device__ __forceinline__ uint32_t tau4(uint32_t a, uint32_t b) {
-    const uint32_t d = __vabsdiffu4(a, b);
-    const uint32_t l = (a + b - d) >> 1;           // a+b-d = 2*min: even, so no byte leaks
-    const uint32_t P = l + 0x7D7D7D7Du;            // bit7: l >= 3
-    const uint32_t Q = l + 0x7F7F7F7Fu;            // bit7: l >= 1
-    const uint32_t U = d + 0x7E7E7E7Eu;            // bit7: d >= 2
-    const uint32_t W = d + 0x7C7C7C7Cu;            // bit7: d >= 4
-    const uint32_t V = d + 0x7A7A7A7Au;            // bit7: d >= 6
-    const uint32_t g1 = P & ~U & 0x80808080u;               // l>=3 and d<2
-    const uint32_t t2 = P & ~V & 0x80808080u;               // l>=3 and d<6
-    const uint32_t t1 = Q & ~W & 0x80808080u;               // l>=1 and d<4
-    const uint32_t g2 = t2 | (t1 & ~P);                     // ... and l<=2
-    return l - (g1 >> 7) - (g2 >> 7);
+// a*m + c on the FMA pipe
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t m, uint32_t c) { return a * m + c; }
+// LOP3 with an explicit truth table (a = 0xF0, b = 0xCC, c = 0xAA).  Written as PTX so ptxas does
+// not fold a NOT into a neighbouring add (it rewrites ~(d + k) as -d - k - 1, costing a negate).
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return r;
+}
+template <uint32_t LUT, uint32_t C>
+__device__ __forceinline__ uint32_t lop3i(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "n"(C), "n"(LUT));
+    return r;
+}
+// max(min(a + b, c), 0) per signed 16-bit lane (DPX VIADDMNMX.S16x2.RELU)
+__device__ __forceinline__ uint32_t relu_min(uint32_t a, uint32_t b, uint32_t c) {
+    return __viaddmin_s16x2_relu(a, b, c);
 }
 
-// zero-extend bytes {0,2} / {1,3} into 16-bit lanes
-__device__ __forceinline__ uint32_t lo16z(uint32_t w) { return prmt(w, 0u, 0x4240u); }
-__device__ __forceinline__ uint32_t hi16z(uint32_t w) { return prmt(w, 0u, 0x4341u); }
-// sign-extend bytes {0,2} / {1,3} into 16-bit lanes
-__device__ __forceinline__ uint32_t lo16s(uint32_t w) { return prmt(w, 0u, 0xA280u); }
-__device__ __forceinline__ uint32_t hi16s(uint32_t w) { return prmt(w, 0u, 0xB391u); }
+// Algorithm 1 (P:119-132) on 4 byte lanes, inputs already clamped to [0, 63].
+//   d = |a-b|, l = min(a,b) = (a+b-d)/2
+//   tau = l - c,  c = [l>=3]([d<2] + [d<6]) + [1<=l<=2][d<4]      (l = 0 -> 0)
+// Each comparison v >= k is bit 6 of v + (64 - k), clean because v <= 63 (no carry leaves
+// the byte).  The two correction flags g1, g2 sit at bit 6, so g1 + g2 <= 0x80 never carries
+// and c = (g1 + g2) >> 6.  tau >= 0 in every lane, so l - c never borrows.
+__device__ __forceinline__ uint32_t tau4(uint32_t a, uint32_t b, const Konst& K) {
+    const uint32_t d = __vabsdiffu4(a, b);                       // ALU
+    const uint32_t l = imad(d, K.m1, imad(a, K.one, b)) >> 1;    // 2 FMA + SHF
+    const uint32_t P = imad(l, K.one, 0x3D3D3D3Du);              // bit6: l >= 3
+    const uint32_t Q = imad(l, K.one, 0x3F3F3F3Fu);              // bit6: l >= 1
+    const uint32_t U = imad(d, K.one, 0x3E3E3E3Eu);              // bit6: d >= 2
+    const uint32_t W = imad(d, K.one, 0x3C3C3C3Cu);              // bit6: d >= 4
+    const uint32_t V = imad(d, K.one, 0x3A3A3A3Au);              // bit6: d >= 6
+    const uint32_t g1 = lop3i<0x20, 0x40404040u>(P, U);          // P & ~U & M: l>=3, d<2
+    const uint32_t t2 = lop3i<0x20, 0x40404040u>(P, V);          // P & ~V & M: l>=3, d<6
+    const uint32_t t1 = lop3i<0x20, 0x40404040u>(Q, W);          // Q & ~W & M: l>=1, d<4
+    const uint32_t g2 = lop3<0xF4>(t2, t1, P);                   // t2 | (t1 & ~P): ... l<=2
+    const uint32_t c = imad(g1, K.one, g2) >> 6;
+    return imad(c, K.m1, l);
+}
+
+// sign-extend bytes {1,3} into 16-bit lanes / zero-extend bytes {1,3}
+__device__ __forceinline__ uint32_t hi16s(uint32_t w) { return prmt<0xB391u>(w, 0u); }
+__device__ __forceinline__ uint32_t hi16z(uint32_t w) { return prmt<0x4341u>(w, 0u); }
 // pack the low bytes of two 16x2 words back into frame order {0,1,2,3}
-__device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi) { return prmt(lo, hi, 0x6240u); }
+__device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi) { return prmt<0x6240u>(lo, hi); }
 // byte mask 0xFF where bit 7 of the byte is set
-__device__ __forceinline__ uint32_t bmask7(uint32_t w) { return prmt(w, 0u, 0xBA98u); }
+__device__ __forceinline__ uint32_t bmask7(uint32_t w) { return prmt<0xBA98u>(w, 0u); }
 
 // syndrome nibble (bit f = frame f) -> flag at bit 6 / bit 7 of byte f
 __device__ __forceinline__ uint32_t nib_to_bit6(uint32_t nib) { return (nib * 0x08102040u) & 0x40404040u; }
