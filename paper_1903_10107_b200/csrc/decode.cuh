@@ -106,11 +106,14 @@ __device__ __forceinline__ uint32_t& w4(uint4& v, int i) { return i == 0 ? v.x :
 
 // One check row r of a block row with D edges (layered update, Alg. 1/2).
 //   et   : the row's D (cb, s) entries;  Lrow : this row's Dp words;  nib : target syndrome bits
-template <int D, bool ESM, bool POW2>
+template <int D, bool ESM, bool POW2, int KEEP_ADDR_MAX = 10>
 __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, uint32_t r4, uint32_t zm4,
                                            unsigned char* Eb, uint32_t* __restrict__ Lrow, uint32_t nib,
                                            bool first, const Konst& K) {
     constexpr int NV = (D + 3) / 4;
+    // High degrees recompute each E address in the emit phase (one smem table load + IMAD + LOP3)
+    // instead of holding D addresses in registers through the forward/backward passes.
+    constexpr bool KEEP_ADDR = D <= KEEP_ADDR_MAX;
     uint4 S[NV];
     uint32_t addr[D];
     EdgeIn in[D];
@@ -132,10 +135,18 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
     // edges are emitted from k = D-1 down to 0, so a 128-bit group of new messages is complete
     // (and stored) once its lowest edge is done
     auto emit = [&](int k, uint32_t o) {
-        const uint32_t ew = ldE<ESM>(Eb, addr[k]);
+        uint32_t a;
+        if constexpr (KEEP_ADDR) {
+            a = addr[k];
+        } else {
+            int2 e;   // volatile: force the reload so ptxas does not keep the table entry live
+            asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"((uint32_t)__cvta_generic_to_shared(et + k)));
+            a = Addr<POW2>::at(e, r4, zm4, Z, K);
+        }
+        const uint32_t ew = ldE<ESM>(Eb, a);
         uint32_t eo;
         w4(S[k >> 2], k & 3) = edge_out(o, Q ^ in[k].cw, in[k], ew, K, eo);
-        stE<ESM>(Eb, addr[k], eo);
+        stE<ESM>(Eb, a, eo);
         if ((k & 3) == 0) st4(Lrow + k, S[k >> 2]);
     };
     if constexpr (D == 1) {
@@ -158,6 +169,21 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         }
         emit(0, B);
     }
+}
+
+// Stopping criterion for one check row: bit 7 of the result is set in lane f iff the row's
+// parity of hard decisions differs from the target bit.  Hard decision = (E < 0) = NOT bit 7 of
+// (E'' + 1), so the parity of the d decisions is bit 7 of XOR(E''_k + 1) ^ (d odd ? 0x80 : 0).
+template <int D, bool POW2>
+__device__ __forceinline__ uint32_t syndrome_row(const int2* __restrict__ et, int Z, uint32_t r4, uint32_t zm4,
+                                                 const unsigned char* Eb, uint32_t nib, const Konst& K) {
+    uint32_t e[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) e[k] = ldE<true>(Eb, Addr<POW2>::at(et[k], r4, zm4, Z, K));
+    uint32_t acc = nib_to_bit7(nib) ^ ((D & 1) ? 0x80808080u : 0u);
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc ^= imad(e[k], K.one, 0x01010101u);
+    return acc;
 }
 
 // Runtime-degree variant (any degree <= 64), same arithmetic; state in local memory.

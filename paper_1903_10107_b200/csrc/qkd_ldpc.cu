@@ -69,7 +69,7 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
     case DD:                                                                                             \
         if constexpr (DD <= DMAX) {                                                                      \
             for (int r = t; r < p.Z; r += p.TG)                                                          \
-                row_update<DD, ESM, POW2>(et, p.Z, 4u * r, zm4, Eb, Lslot + li.z + r * li.w, synI[r], first, K); \
+                row_update<DD, ESM, POW2, (DMAX <= 8 ? 4 : 10)>(et, p.Z, 4u * r, zm4, Eb, Lslot + li.z + r * li.w, synI[r], first, K); \
             return;                                                                                      \
         }                                                                                                \
         break;
@@ -90,7 +90,7 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
 
 // per-lane syndrome violation mask (bit f set = frame f violates some parity check),
 // group-uniform.  Hard decision bit = (E < 0) = NOT bit 7 of (E'' + 1), E'' = E + 127 (R9).
-template <bool ESM, bool POW2>
+template <int DMAX, bool ESM, bool POW2>
 __device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int4* s_layer, const int2* s_edge,
                                                   const unsigned char* Eb, const uint8_t* sSyn, int t,
                                                   uint32_t* flags, int& chk, int bar, const Konst& K) {
@@ -99,12 +99,34 @@ __device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int4
     for (int I = 0; I < p.Mb; ++I) {
         const int4 li = s_layer[I];
         const int2* et = s_edge + li.y;
-        const uint32_t par = (li.x & 1) ? 0x80808080u : 0u;
-        for (int r = t; r < p.Z; r += p.TG) {
-            uint32_t acc = nib_to_bit7(sSyn[I * p.Z + r]) ^ par;
-            for (int k = 0; k < li.x; ++k)
-                acc ^= imad(ldE<ESM>(Eb, Addr<POW2>::at(et[k], 4u * r, zm4, p.Z, K)), K.one, 0x01010101u);
-            v |= acc;
+        const uint8_t* synI = sSyn + I * p.Z;
+        bool done = false;
+        if constexpr (DMAX > 0 && ESM) {
+            switch (li.x) {
+#define QKD_SCASE(DD)                                                                                  \
+    case DD:                                                                                           \
+        if constexpr (DD <= DMAX) {                                                                    \
+            for (int r = t; r < p.Z; r += p.TG) v |= syndrome_row<DD, POW2>(et, p.Z, 4u * r, zm4, Eb, synI[r], K); \
+            done = true;                                                                               \
+        }                                                                                              \
+        break;
+                QKD_SCASE(1) QKD_SCASE(2) QKD_SCASE(3) QKD_SCASE(4) QKD_SCASE(5) QKD_SCASE(6) QKD_SCASE(7)
+                QKD_SCASE(8) QKD_SCASE(9) QKD_SCASE(10) QKD_SCASE(11) QKD_SCASE(12) QKD_SCASE(13)
+                QKD_SCASE(14) QKD_SCASE(15) QKD_SCASE(16) QKD_SCASE(17) QKD_SCASE(18) QKD_SCASE(19)
+                QKD_SCASE(20)
+#undef QKD_SCASE
+                default:
+                    break;
+            }
+        }
+        if (!done) {
+            const uint32_t par = (li.x & 1) ? 0x80808080u : 0u;
+            for (int r = t; r < p.Z; r += p.TG) {
+                uint32_t acc = nib_to_bit7(synI[r]) ^ par;
+                for (int k = 0; k < li.x; ++k)
+                    acc ^= imad(ldE<ESM>(Eb, Addr<POW2>::at(et[k], 4u * r, zm4, p.Z, K)), K.one, 0x01010101u);
+                v |= acc;
+            }
         }
     }
     v &= 0x80808080u;
@@ -247,7 +269,7 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
         uint32_t active = (1u << nl) - 1u;
         int chk = 0;
         if (p.early_stop) {   // iteration-0 check (R10)
-            const uint32_t viol = syndrome_viol<ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
+            const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
             const uint32_t done = active & ~viol;
             if (done) {
                 finalize(p, s_layer, Eslot, Lslot, f0, done, 0, done, true, t);
@@ -265,7 +287,7 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
                 group_bar(bar, p.TG);
             }
             if (p.early_stop) {
-                const uint32_t viol = syndrome_viol<ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
+                const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
                 const uint32_t done = active & ~viol;
                 if (done) {
                     finalize(p, s_layer, Eslot, Lslot, f0, done, it, done, false, t);
@@ -277,7 +299,7 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
         if (active) {   // ran out of iterations (or early_stop = 0): state after sweep T (R12)
             uint32_t succ = 0;
             if (!p.early_stop)
-                succ = active & ~syndrome_viol<ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
+                succ = active & ~syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
             finalize(p, s_layer, Eslot, Lslot, f0, active, it, succ, it == 0, t);
         }
         group_bar(bar, p.TG);
