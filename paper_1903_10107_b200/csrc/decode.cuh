@@ -132,8 +132,19 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
     // s_i ^ XOR_{j != k} [x_j < 0] = s_i ^ ((D-1)&1) ^ P ^ nonneg_k   (bit 6)
     const uint32_t Q = P ^ nib_to_bit6(nib) ^ (((D - 1) & 1) ? 0x40404040u : 0u);
     // emit edge k as soon as its leave-one-out magnitude is known (keeps the live set small)
-    // edges are emitted from k = D-1 down to 0, so a 128-bit group of new messages is complete
-    // (and stored) once its lowest edge is done
+    // Leave-one-out by the forward/backward schedule of R6, evaluated meet-in-the-middle: the
+    // forward chain over edges [0, H) and the backward chain over [H, D) run concurrently, then
+    // each continues across the other half while emitting outputs.  Every tau has exactly the
+    // arguments of the plain F/B schedule (F_k = tau(F_{k-1}, m_k), B_k = tau(m_k, B_{k+1}),
+    // o_k = tau(F_{k-1}, B_{k+1})), so results are identical; two independent chains double the ILP.
+    constexpr int H = D / 2;
+    auto step_of = [](int k) { return k >= H ? 2 * (k - H) : 2 * (H - 1 - k) + 1; };   // emission order
+    auto last_of_group = [&](int k) {   // is k the last-emitted edge of its 128-bit group?
+        int best = -1, arg = -1;
+        for (int q = k & ~3; q < (k & ~3) + 4 && q < D; ++q)
+            if (step_of(q) > best) { best = step_of(q); arg = q; }
+        return arg == k;
+    };
     auto emit = [&](int k, uint32_t o) {
         uint32_t a;
         if constexpr (KEEP_ADDR) {
@@ -147,7 +158,7 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         uint32_t eo;
         w4(S[k >> 2], k & 3) = edge_out(o, Q ^ in[k].cw, in[k], ew, K, eo);
         stE<ESM>(Eb, a, eo);
-        if ((k & 3) == 0) st4(Lrow + k, S[k >> 2]);
+        if (D <= 2 ? (k == 0) : last_of_group(k)) st4(Lrow + (k & ~3), S[k >> 2]);
     };
     if constexpr (D == 1) {
         emit(0, 0x3F3F3F3Fu);                       // empty box-plus -> MSG_max (R6)
@@ -155,19 +166,33 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         emit(1, edge_mag(in[0].cw, K));
         emit(0, edge_mag(in[1].cw, K));
     } else {
-        // forward/backward leave-one-out in ascending block column (R6)
-        uint32_t F[D - 1];
+        uint32_t F[H], B[D];                        // F_0..F_{H-1}; B_H..B_{D-1}
         F[0] = edge_mag(in[0].cw, K);
+        B[D - 1] = edge_mag(in[D - 1].cw, K);
 #pragma unroll
-        for (int k = 1; k <= D - 2; ++k) F[k] = tau4(F[k - 1], edge_mag(in[k].cw, K), K);
-        emit(D - 1, F[D - 2]);
-        uint32_t B = edge_mag(in[D - 1].cw, K);
-#pragma unroll
-        for (int k = D - 2; k >= 1; --k) {
-            emit(k, tau4(F[k - 1], B, K));
-            B = tau4(edge_mag(in[k].cw, K), B, K);
+        for (int j = 1; j < D; ++j) {               // phase 1: both chains, interleaved
+            if (j <= H - 1) F[j] = tau4(F[j - 1], edge_mag(in[j].cw, K), K);
+            const int kb = D - 1 - j;
+            if (kb >= H) B[kb] = tau4(edge_mag(in[kb].cw, K), B[kb + 1], K);
         }
-        emit(0, B);
+        uint32_t f = F[H - 1], b = B[H];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {               // phase 2: continue across, emitting
+            const int kf = H + j;                   // forward: o_kf = tau(F_{kf-1}, B_{kf+1})
+            if (kf <= D - 2) {
+                emit(kf, tau4(f, B[kf + 1], K));
+                f = tau4(f, edge_mag(in[kf].cw, K), K);
+            } else if (kf == D - 1) {
+                emit(D - 1, f);                     // o_{D-1} = F_{D-2}
+            }
+            const int kb = H - 1 - j;               // backward: o_kb = tau(F_{kb-1}, B_{kb+1})
+            if (kb >= 1) {
+                emit(kb, tau4(F[kb - 1], b, K));
+                b = tau4(edge_mag(in[kb].cw, K), b, K);
+            } else if (kb == 0) {
+                emit(0, b);                         // o_0 = B_1
+            }
+        }
     }
 }
 
