@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqkdldpc.so")
+LIB_PATH = os.environ.get("QKD_LIB") or os.path.join(_HERE, "libqkdldpc.so")  # QKD_LIB: an alternative in-tree build (A/B timing)
 _lib = None
 
 QKD_OK = 0

@@ -12,11 +12,23 @@
 #pragma once
 #include "swar.cuh"
 
+#ifndef QKD_SPLIT_REMAG
+#define QKD_SPLIT_REMAG 0
+#endif
+#ifndef QKD_TAUC
+#define QKD_TAUC 1
+#endif
+#ifndef QKD_SPLIT_KREG
+#define QKD_SPLIT_KREG 1
+#endif
+
 namespace qkd {
 
 struct DecParams {
     const int4* layer;        // [Mb] (degree, first base edge, L offset in words, Dp)
     const int2* edge;         // [nbase] (J*Z, shift)
+    const int* soff;          // [Mb] split-table offset of block row I (entries; split layout only)
+    int nsplit;               // split-table entries per slot (sum over I of 2 * HB_I)
     int Mb, Z, nbase, n, m, mb8, nb8;
     long long n_edges;        // canonical message count (nbase * Z)
     long long ws_words;       // workspace words per slot (sum over I of Z * Dp_I)
@@ -83,6 +95,35 @@ __device__ __forceinline__ EdgeIn edge_in(uint32_t e, uint32_t s, const Konst& K
 // check-node magnitude min(|x|, 63) (MSG_max = 63)
 __device__ __forceinline__ uint32_t edge_mag(uint32_t cw, const Konst& K) { return __vabsdiffu4(cw, K.c63); }
 
+// complement form 63 - min(|x|, 63) of the same magnitude (input of tau4c)
+__device__ __forceinline__ uint32_t edge_magc(uint32_t cw, const Konst& K) {
+    return imad(__vabsdiffu4(cw, K.c63), K.m1, 0x3F3F3F3Fu);
+}
+
+// The same value by a different instruction sequence (immediate operand, IADD3): ptxas cannot
+// merge it with edge_magc, so the split kernel recomputes it instead of keeping it live.
+__device__ __forceinline__ uint32_t edge_magc_alt(uint32_t cw) { return 0x3F3F3F3Fu - __vabsdiffu4(cw, 0x3F3F3F3Fu); }
+
+// Emit for the split kernel, from the pre-layer E word ew and the old message word s_old only
+// (no 16-bit X words kept from edge_in): with oc = 63 - o and M = 0xFF where L_new < 0,
+//   S_new = 64 - L_new = (oc ^ (M & 0x7F)) + [L_new >= 0]          (127 - oc or oc + 1)
+//   E_new'' = clamp(ew + S_old - S_new, 0, 254) = clamp(E + L_new - L_old, -127, 127) + 127,
+// with d = S_old - S_new + 128 in [2, 254] per byte and the sum in 16-bit lanes; Algorithm 2
+// keeps ew where |E| = 127.  Returns S_new.
+__device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t negf, uint32_t s_old, uint32_t ew,
+                                               const Konst& K, uint32_t& e_out) {
+    const uint32_t M = bmask7(imad(negf, K.two, 0u));             // 0xFF where L_new < 0
+    const uint32_t x1 = lop3i<0x78, 0x7F7F7F7Fu>(oc, M);          // oc ^ (M & 0x7F)
+    const uint32_t sn = imad(lop3i<0x0A, 0x01010101u>(M, 0u), K.one, x1);   // + (~M & 1)
+    const uint32_t d = s_old + 0x80808080u - sn;                  // IADD3, exact per byte
+    const uint32_t hi = imad(hi16z(ew), K.one, hi16z(d));         // lanes {1,3}: ew + d
+    const uint32_t lo = imad(hi, K.m256, imad(ew, K.one, d));     // lanes {0,2}
+    const uint32_t enew = pack16(relu_min(lo, K.b128, 0x00FE00FEu), relu_min(hi, K.b128, 0x00FE00FEu));
+    const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
+    e_out = lop3<0xCA>(G, ew, enew);
+    return sn;
+}
+
 // Given the leave-one-out magnitude o, the sign flag (bit 6 of negf = 1 -> L_new < 0), the
 // edge's X words and the pre-layer E word: returns the new S word (stored) and writes the new
 // E word (Algorithm 2 guard on |E| = E_max, Eq.(9) saturated to +-127).
@@ -98,6 +139,21 @@ __device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t negf, const Ed
     const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);                              // G ? ew : enew
     return imad(Tb, K.m1, 0x01010100u);                           // 128 - T = 64 - L_new
+}
+
+// edge_out with the leave-one-out magnitude in complement form oc = 63 - o (tau4c output):
+// o & M = (oc ^ 63) & M is still one LOP3 and o + 0xC0 = 0xFF - oc one IMAD, so nothing is added.
+__device__ __forceinline__ uint32_t edge_out_c(uint32_t oc, uint32_t negf, const EdgeIn& in, uint32_t ew,
+                                               const Konst& K, uint32_t& e_out) {
+    const uint32_t M = bmask7(imad(negf, K.two, 0u));             // 0xFF where L_new < 0
+    const uint32_t om = lop3i<0x48, 0x3F3F3F3Fu>(oc, M);          // (oc ^ 63) & M = o & M
+    const uint32_t Tb = imad(om, K.m2, imad(oc, K.m1, 0xFFFFFFFFu));   // 255 - oc - 2 om = 192 + L_new
+    const uint32_t thi = hi16s(Tb);
+    const uint32_t tlo = imad(imad(thi, K.m256, Tb), K.one, 0xFFFFFF00u);
+    const uint32_t enew = pack16(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu));
+    const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
+    e_out = lop3<0xCA>(G, ew, enew);
+    return imad(Tb, K.m1, 0x01010100u);                           // 64 - L_new
 }
 
 __device__ __forceinline__ uint4 ld4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
@@ -156,43 +212,138 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         }
         const uint32_t ew = ldE<ESM>(Eb, a);
         uint32_t eo;
+#if QKD_TAUC
+        w4(S[k >> 2], k & 3) = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
+#else
         w4(S[k >> 2], k & 3) = edge_out(o, Q ^ in[k].cw, in[k], ew, K, eo);
+#endif
         stE<ESM>(Eb, a, eo);
         if (D <= 2 ? (k == 0) : last_of_group(k)) st4(Lrow + (k & ~3), S[k >> 2]);
     };
+#if QKD_TAUC
+    // complement form (tau4c / edge_magc / edge_out_c): two instructions fewer per tau
+#define QKD_TAU tau4c
+#define QKD_MAG edge_magc
+#define QKD_O63 0u
+#else
+#define QKD_TAU tau4
+#define QKD_MAG edge_mag
+#define QKD_O63 0x3F3F3F3Fu
+#endif
     if constexpr (D == 1) {
-        emit(0, 0x3F3F3F3Fu);                       // empty box-plus -> MSG_max (R6)
+        emit(0, QKD_O63);                           // empty box-plus -> MSG_max (R6)
     } else if constexpr (D == 2) {
-        emit(1, edge_mag(in[0].cw, K));
-        emit(0, edge_mag(in[1].cw, K));
+        emit(1, QKD_MAG(in[0].cw, K));
+        emit(0, QKD_MAG(in[1].cw, K));
     } else {
         uint32_t F[H], B[D];                        // F_0..F_{H-1}; B_H..B_{D-1}
-        F[0] = edge_mag(in[0].cw, K);
-        B[D - 1] = edge_mag(in[D - 1].cw, K);
+        F[0] = QKD_MAG(in[0].cw, K);
+        B[D - 1] = QKD_MAG(in[D - 1].cw, K);
 #pragma unroll
         for (int j = 1; j < D; ++j) {               // phase 1: both chains, interleaved
-            if (j <= H - 1) F[j] = tau4(F[j - 1], edge_mag(in[j].cw, K), K);
+            if (j <= H - 1) F[j] = QKD_TAU(F[j - 1], QKD_MAG(in[j].cw, K), K);
             const int kb = D - 1 - j;
-            if (kb >= H) B[kb] = tau4(edge_mag(in[kb].cw, K), B[kb + 1], K);
+            if (kb >= H) B[kb] = QKD_TAU(QKD_MAG(in[kb].cw, K), B[kb + 1], K);
         }
         uint32_t f = F[H - 1], b = B[H];
 #pragma unroll
         for (int j = 0; j < D; ++j) {               // phase 2: continue across, emitting
             const int kf = H + j;                   // forward: o_kf = tau(F_{kf-1}, B_{kf+1})
             if (kf <= D - 2) {
-                emit(kf, tau4(f, B[kf + 1], K));
-                f = tau4(f, edge_mag(in[kf].cw, K), K);
+                emit(kf, QKD_TAU(f, B[kf + 1], K));
+                f = QKD_TAU(f, QKD_MAG(in[kf].cw, K), K);
             } else if (kf == D - 1) {
                 emit(D - 1, f);                     // o_{D-1} = F_{D-2}
             }
             const int kb = H - 1 - j;               // backward: o_kb = tau(F_{kb-1}, B_{kb+1})
             if (kb >= 1) {
-                emit(kb, tau4(F[kb - 1], b, K));
-                b = tau4(edge_mag(in[kb].cw, K), b, K);
+                emit(kb, QKD_TAU(F[kb - 1], b, K));
+                b = QKD_TAU(QKD_MAG(in[kb].cw, K), b, K);
             } else if (kb == 0) {
                 emit(0, b);                         // o_0 = B_1
             }
         }
+    }
+#undef QKD_TAU
+#undef QKD_MAG
+#undef QKD_O63
+}
+
+// ---------------------------------------------------------------------------------------------
+// Split row: the D edges of check row r are shared by a lane pair (lanes 2i, 2i+1 of one warp),
+// which halves the per-thread state so a CTA can run 1024 threads (32 warps per SM).
+//   side A (even lane): edges k = 0 .. HA-1, local j = k            HA = D / 2
+//   side B (odd lane):  edges k = D-1 .. HA,  local j = D-1-k        HB = D - HA
+// Each side first runs one chain of the forward/backward schedule of R6 over its own edges
+// (A: F_0..F_{HA-1}, B: B_{D-1}..B_{HA}; tau is symmetric), the two boundary values cross once
+// by shuffle, and each side then continues the other chain across its own edges, emitting
+// o_k = tau(F_{k-1}, B_{k+1}) -- every tau has the arguments of the plain schedule, so results
+// are identical.  The sign product of Eq.(1) is the XOR of both halves (one more shuffle).
+// Messages: a lane owns words [side*WA, side*WA + n) of the row (WA = roundup2(HA)) and moves
+// them with 64-bit loads/stores.  Magnitudes run in complement form (tau4c).
+//   et2 : 2*HB table entries, [2j + side] = the lane's j-th edge (side A's empty slot of an odd
+//         degree repeats side B's entry so its load stays in bounds; its results are unused).
+// All 32 lanes of the warp call this (the shuffles need them); `act` = the row exists.
+template <int D, bool POW2>
+__device__ __forceinline__ void row_update_split(const int2* __restrict__ et2, int Z, uint32_t r4, uint32_t zm4,
+                                                 unsigned char* Eb, uint32_t* __restrict__ Lh, uint32_t nib,
+                                                 bool first, bool act, int side, const Konst& K) {
+    constexpr int HA = D / 2, HB = D - HA, NW = (HB + 1) / 2;
+    const int n = side ? HB : HA;
+    uint2 S[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        if (first || !act || 2 * w >= n) S[w] = make_uint2(0x40404040u, 0x40404040u);
+        else S[w] = *reinterpret_cast<const uint2*>(Lh + 2 * w);
+    }
+    auto sw = [&](int j) -> uint32_t& { return (j & 1) ? S[j >> 1].y : S[j >> 1].x; };
+    // E address of local edge j: the table entry is re-read (volatile) at both uses, so ptxas
+    // neither keeps HB addresses live nor hoists the loop-invariant entries and spills them
+    auto addr = [&](int j) -> uint32_t {
+        int2 e;
+        asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y)
+                     : "r"((uint32_t)__cvta_generic_to_shared(et2 + 2 * j + side)));
+        return Addr<POW2>::at(e, r4, zm4, Z, K);
+    };
+    uint32_t cw[HB];
+    uint32_t P = 0;
+#pragma unroll
+    for (int j = 0; j < HB; ++j) {
+        cw[j] = edge_in(ldE<true>(Eb, addr(j)), sw(j), K).cw;
+        if (HA == HB || j < n) P ^= cw[j];
+    }
+    P ^= __shfl_xor_sync(0xffffffffu, P, 1);
+    const uint32_t Q = P ^ nib_to_bit6(nib) ^ (((D - 1) & 1) ? 0x40404040u : 0u);
+    auto emit = [&](int j, uint32_t oc) {
+        const uint32_t aj = addr(j);
+        const uint32_t ew = ldE<true>(Eb, aj);        // pre-layer E (no other row of the layer touches it)
+        uint32_t eo;
+        const uint32_t sn = edge_out_s(oc, Q ^ cw[j], sw(j), ew, K, eo);
+        sw(j) = sn;
+        if (act) {
+            stE<true>(Eb, aj, eo);
+            if ((j & 1) == 0) *reinterpret_cast<uint2*>(Lh + j) = S[j >> 1];   // j+1 was emitted before j
+        }
+    };
+    if constexpr (D == 1) {
+        if (side) emit(0, 0u);                      // empty box-plus -> MSG_max = 63 (R6)
+    } else {
+        uint32_t ch[HB];
+        ch[0] = edge_magc(cw[0], K);
+#pragma unroll
+        for (int j = 1; j < HB; ++j)
+            if (HA == HB || j < n) ch[j] = tau4c(ch[j - 1], edge_magc(cw[j], K), K);
+        const uint32_t send = (HA == HB || side) ? ch[HB - 1] : ch[HA - 1];
+        uint32_t acc = __shfl_xor_sync(0xffffffffu, send, 1);   // A: B_HA, B: F_{HA-1}
+#pragma unroll
+        for (int j = HB - 1; j >= 1; --j) {
+            if (HA == HB || j < n) {
+                const uint32_t o = tau4c(ch[j - 1], acc, K);       // o_k = tau(F_{k-1}, B_{k+1})
+                acc = tau4c(edge_magc_alt(cw[j]), acc, K);         // continue the other chain
+                emit(j, o);
+            }
+        }
+        emit(0, acc);                                          // A: o_0 = B_1, B: o_{D-1} = F_{D-2}
     }
 }
 

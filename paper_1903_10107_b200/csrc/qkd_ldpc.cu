@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -48,6 +49,12 @@ struct qkd_code {
     uint8_t* d_payload = nullptr;  // packed payload mask or null (= all payload)
     bool has_short = false;
     int device = 0;
+    // split layout (decode variant 5, lane-pair rows): per block row, side A's words then side B's,
+    // row stride roundup2(HA) + roundup2(HB); the split table holds 2*HB entries per block row
+    bool split = false;
+    std::vector<int> soff;
+    int nsplit = 0;
+    int* d_soff = nullptr;
 };
 
 // --------------------------------------------------------------------------------------
@@ -58,12 +65,35 @@ namespace {
 
 constexpr int kFramesPerGroup = 4;
 
-template <int DMAX, bool ESM, bool POW2>
+template <int DMAX, bool ESM, bool POW2, bool SPLIT>
 __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, const int2* et, int t,
                                            unsigned char* Eb, uint32_t* Lslot, const uint8_t* synI, bool first,
                                            const Konst& K) {
     const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
-    if constexpr (DMAX > 0) {
+    if constexpr (SPLIT) {
+        // lane pairs: warp-uniform trip count (the shuffles need all 32 lanes), 16 rows per warp pass
+        const int side = t & 1, pairs = p.TG >> 1, wa = ((li.x >> 1) + 1) & ~1;
+        switch (li.x) {
+#define QKD_SCASE2(DD)                                                                                   \
+    case DD:                                                                                             \
+        for (int rb = (t >> 1) & ~15; rb < p.Z; rb += pairs) {                                           \
+            const int r0 = rb + ((t >> 1) & 15);                                                         \
+            const bool act = r0 < p.Z;                                                                   \
+            const int r = act ? r0 : p.Z - 1;                                                            \
+            row_update_split<DD, POW2>(et, p.Z, 4u * r, zm4, Eb, Lslot + li.z + r * li.w + side * wa, synI[r], \
+                                       first, act, side, K);                                            \
+        }                                                                                                \
+        return;
+            QKD_SCASE2(1) QKD_SCASE2(2) QKD_SCASE2(3) QKD_SCASE2(4) QKD_SCASE2(5) QKD_SCASE2(6)
+            QKD_SCASE2(7) QKD_SCASE2(8) QKD_SCASE2(9) QKD_SCASE2(10) QKD_SCASE2(11) QKD_SCASE2(12)
+            QKD_SCASE2(13) QKD_SCASE2(14) QKD_SCASE2(15) QKD_SCASE2(16) QKD_SCASE2(17) QKD_SCASE2(18)
+            QKD_SCASE2(19) QKD_SCASE2(20)
+#undef QKD_SCASE2
+            default:
+                break;
+        }
+        __trap();
+    } else if constexpr (DMAX > 0) {
         switch (li.x) {
 #define QKD_CASE(DD)                                                                                     \
     case DD:                                                                                             \
@@ -166,8 +196,13 @@ __device__ void finalize(const DecParams& p, const int4* s_layer, const uint32_t
                 for (int q = t; q < cnt; q += p.TG) {
                     const int k = q / p.Z, r = q - k * p.Z;
                     const long long e = (long long)(li.y + k) * p.Z + r;     // canonical edge order
+                    int wk = k;   // word of canonical edge k inside the row (split: side A, then side B)
+                    if (p.soff) {
+                        const int ha = li.x >> 1;
+                        wk = k < ha ? k : ((ha + 1) & ~1) + (li.x - 1 - k);
+                    }
                     lrow[e] = first ? (int8_t)0
-                                    : (int8_t)(64 - (int)((Lslot[li.z + r * li.w + k] >> (8 * f)) & 0xFFu));
+                                    : (int8_t)(64 - (int)((Lslot[li.z + r * li.w + wk] >> (8 * f)) & 0xFFu));
                 }
             }
         }
@@ -184,19 +219,36 @@ __device__ void finalize(const DecParams& p, const int4* s_layer, const uint32_t
     }
 }
 
-template <int DMAX, bool ESM, bool POW2>
-__global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1)
+template <int DMAX, bool ESM, bool POW2, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1)
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const Konst K = p.K.in_regs();
+    const Konst K = (SPLIT && !QKD_SPLIT_KREG) ? p.K : p.K.in_regs();
     // tables: layer info, then one edge table per slot with the slot's E base folded in
     int4* s_layer = reinterpret_cast<int4*>(smem + p.tab_off);
     int2* s_edges = reinterpret_cast<int2*>(s_layer + p.Mb);
-    for (int i = threadIdx.x; i < p.Mb; i += blockDim.x) s_layer[i] = p.layer[i];
+    int2* s_split = s_edges + p.GPC * p.nbase;   // [GPC][nsplit] lane-pair order (SPLIT only)
+    int* s_soff = reinterpret_cast<int*>(s_split + (SPLIT ? p.GPC * p.nsplit : 0));   // [Mb] (SPLIT only)
+    for (int i = threadIdx.x; i < p.Mb; i += blockDim.x) {
+        s_layer[i] = p.layer[i];
+        if (SPLIT) s_soff[i] = p.soff[i];
+    }
     for (int i = threadIdx.x; i < p.GPC * p.nbase; i += blockDim.x) {
         const int sl = i / p.nbase;
         const int2 e = p.edge[i - sl * p.nbase];
         s_edges[i] = POW2 ? make_int2(sl * p.slot_bytes + 4 * e.x, 4 * e.y) : e;
+    }
+    if constexpr (SPLIT) {
+        for (int I = 0; I < p.Mb; ++I) {
+            const int4 li = p.layer[I];
+            const int ha = li.x >> 1, hb = li.x - ha;
+            for (int i = threadIdx.x; i < p.GPC * 2 * hb; i += blockDim.x) {
+                const int sl = i / (2 * hb), q = i - sl * 2 * hb, j = q >> 1, side = q & 1;
+                const int k = (side || j >= ha) ? li.x - 1 - j : j;
+                const int2 e = p.edge[li.y + k];
+                s_split[sl * p.nsplit + p.soff[I] + q] = POW2 ? make_int2(sl * p.slot_bytes + 4 * e.x, 4 * e.y) : e;
+            }
+        }
     }
     __syncthreads();
 
@@ -204,6 +256,7 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
     const int t = threadIdx.x - slot * p.TG;
     const int bar = 1 + slot;
     const int2* s_edge = s_edges + slot * p.nbase;
+    const int2* s_edge2 = s_split + slot * p.nsplit;
     unsigned char* sbase = smem + (size_t)slot * p.slot_bytes;
     const long long gslot = (long long)blockIdx.x * p.GPC + slot;
     uint32_t* Eslot = ESM ? reinterpret_cast<uint32_t*>(sbase) : p.Ews + gslot * (long long)p.n;
@@ -283,7 +336,8 @@ __global__ void __launch_bounds__(DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1
             const bool first = it == 1;
             for (int I = 0; I < p.Mb; ++I) {
                 const int4 li = s_layer[I];
-                layer_pass<DMAX, ESM, POW2>(p, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z, first, K);
+                layer_pass<DMAX, ESM, POW2, SPLIT>(p, li, SPLIT ? s_edge2 + s_soff[I] : s_edge + li.y, t, Eb, Lslot,
+                                                   sSyn + I * p.Z, first, K);
                 group_bar(bar, p.TG);
             }
             if (p.early_stop) {
@@ -405,7 +459,12 @@ __global__ void tau_table_kernel(uint8_t* out, Konst K) {
         const uint32_t b = (uint32_t)(4 * w) | ((uint32_t)(4 * w + 1) << 8) | ((uint32_t)(4 * w + 2) << 16) |
                            ((uint32_t)(4 * w + 3) << 24);
         const uint32_t t = tau4(a, b, K);
-        for (int q = 0; q < 4; ++q) out[p * 64 + 4 * w + q] = (uint8_t)(t >> (8 * q));
+        // the complement form used by the split kernel must agree byte for byte (else 0xFF)
+        const uint32_t tc = tau4c(a ^ 0x3F3F3F3Fu, b ^ 0x3F3F3F3Fu, K) ^ 0x3F3F3F3Fu;
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t v = (t >> (8 * q)) & 0xFFu;
+            out[p * 64 + 4 * w + q] = (uint8_t)(v == ((tc >> (8 * q)) & 0xFFu) ? v : 0xFFu);
+        }
     }
 }
 
@@ -438,9 +497,9 @@ DevInfo dev_info(int dev) {
     return cache[dev];
 }
 
-template <int DMAX, bool ESM, bool POW2>
+template <int DMAX, bool ESM, bool POW2, bool SPLIT = false>
 const void* kfun() {
-    return reinterpret_cast<const void*>(&decode_kernel<DMAX, ESM, POW2>);
+    return reinterpret_cast<const void*>(&decode_kernel<DMAX, ESM, POW2, SPLIT>);
 }
 
 const void* kernel_of(int variant, bool pow2) {
@@ -448,12 +507,28 @@ const void* kernel_of(int variant, bool pow2) {
         case 1: return pow2 ? kfun<8, true, true>() : kfun<8, true, false>();
         case 2: return pow2 ? kfun<20, true, true>() : kfun<20, true, false>();
         case 3: return kfun<0, true, false>();
+        case 5: return pow2 ? kfun<20, true, true, true>() : kfun<20, true, false, true>();
         default: return kfun<0, false, false>();
     }
 }
 
 // 1, 2, -1, -2, -256 as kernel arguments: opaque to ptxas, so a*one + c stays an IMAD (FMA pipe)
-Konst runtime_konst() { return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu}; }
+Konst runtime_konst() {
+    return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu, 1u << 26};
+}
+
+// Decode variant of a code on a device (fixed at code creation: the split variant has its own
+// message layout).  1: degree <= 8, smem E; 2: degree <= 20, smem E, one row per thread;
+// 5: degree 9..20, smem E, lane-pair rows; 3: generic smem E; 4: generic global E.
+int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem_optin, bool allow_split) {
+    const long long syn_ctl = ((m + 15) & ~15LL) + 16;
+    const long long tab1 = (long long)Mb * (sizeof(int4) + sizeof(int)) + (long long)nbase * 2 * sizeof(int2) +
+                           (long long)Mb * sizeof(int2);
+    const bool fits = 4LL * n + syn_ctl + tab1 <= smem_optin;
+    if (fits && maxdeg <= 8) return 1;
+    if (fits && maxdeg <= 20) return allow_split ? 5 : 2;
+    return fits ? 3 : 4;
+}
 
 int make_plan(const qkd_code* c, long long F, Plan& pl) {
     int dev = 0;
@@ -463,15 +538,14 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     pl.ngroups = (F + kFramesPerGroup - 1) / kFramesPerGroup;
     const long long syn_ctl = ((c->m + 15) & ~15LL) + 16;
     const long long e_bytes = 4LL * c->n;
-    const long long tab1 = (long long)c->Mb * sizeof(int4) + (long long)c->nbase * sizeof(int2);
-    const bool fits = e_bytes + syn_ctl + tab1 <= di.smem_optin;
-    if (fits && c->maxdeg <= 8) pl.variant = 1;
-    else if (fits && c->maxdeg <= 20) pl.variant = 2;
-    else if (fits) pl.variant = 3;
-    else pl.variant = 4;
-    pl.pow2 = (pl.variant <= 2) && ((c->Z & (c->Z - 1)) == 0);
-    const int tg_max = pl.variant == 1 ? 1024 : (pl.variant == 2 ? 512 : 256);
-    pl.TG = (int)std::min<long long>(((long long)c->Z + 31) / 32 * 32, tg_max);
+    pl.variant = choose_variant(c->Mb, c->n, c->m, c->nbase, c->maxdeg, di.smem_optin, c->split);
+    if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
+    pl.pow2 = (pl.variant <= 2 || pl.variant == 5) && ((c->Z & (c->Z - 1)) == 0);
+    const int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024 : (pl.variant == 2 ? 512 : 256);
+    if (pl.variant == 5)   // two lanes per row, 16 rows per warp
+        pl.TG = (int)std::min<long long>(((long long)c->Z + 15) / 16 * 32, tg_max);
+    else
+        pl.TG = (int)std::min<long long>(((long long)c->Z + 31) / 32 * 32, tg_max);
     pl.e_bytes = pl.variant == 4 ? 0 : (int)e_bytes;
     long long slot = (pl.e_bytes + syn_ctl + 15) & ~15LL;   // 16-byte aligned slots and tables
     if (pl.pow2) {   // slot E bases must be multiples of 4Z for the byte-OR addressing
@@ -479,16 +553,17 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
         slot = (slot + al - 1) / al * al;
     }
     pl.slot_bytes = (int)slot;
-    if (slot + tab1 > di.smem_optin) return fail(QKD_EUNSUP, "frame too long for the shared-memory buffers");
     int gpc = std::min(15, tg_max / pl.TG);
-    while (gpc > 1 && (long long)gpc * (slot + (long long)c->nbase * sizeof(int2)) + c->Mb * sizeof(int4) >
-                          (long long)di.smem_optin)
-        --gpc;
+    const long long per_slot_tab = (long long)(c->nbase + c->nsplit) * sizeof(int2);
+    const long long fixed_tab = (long long)c->Mb * (sizeof(int4) + sizeof(int));
+    if (slot + per_slot_tab + fixed_tab > di.smem_optin)
+        return fail(QKD_EUNSUP, "frame too long for the shared-memory buffers");
+    while (gpc > 1 && (long long)gpc * (slot + per_slot_tab) + fixed_tab > (long long)di.smem_optin) --gpc;
     const long long need = (pl.ngroups + di.sms - 1) / di.sms;
     gpc = (int)std::max<long long>(1, std::min<long long>(gpc, need));
     pl.GPC = gpc;
     pl.tab_off = gpc * pl.slot_bytes;
-    pl.smem = pl.tab_off + (int)(c->Mb * sizeof(int4) + (size_t)gpc * c->nbase * sizeof(int2));
+    pl.smem = pl.tab_off + (int)(fixed_tab + gpc * per_slot_tab);
     const void* k = kernel_of(pl.variant, pl.pow2);
     QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
     int per_sm = 0;
@@ -519,6 +594,25 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
     if (Mb < 1 || Nb <= Mb || Z < 1) return fail(QKD_EINVAL, "need Mb >= 1, Nb > Mb, Z >= 1");
     if ((long long)Nb * Z > (1LL << 30)) return fail(QKD_EUNSUP, "n too large");
     qkd_code* c = new qkd_code();
+    {   // the decode variant (and with it the message layout) is fixed here, per device
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) { delete c; return fail(QKD_ECUDA, "no CUDA device"); }
+        const DevInfo di = dev_info(dev);
+        if (!di.ok) { delete c; return fail(QKD_ECUDA, "cannot query device attributes"); }
+        int nb = 0, md = 0;
+        for (int I = 0; I < Mb; ++I) {
+            int d = 0;
+            for (int J = 0; J < Nb; ++J) d += base_shifts[(size_t)I * Nb + J] >= 0;
+            nb += d;
+            md = std::max(md, d);
+        }
+        // QKD_SPLIT=1 in the environment at code creation selects the lane-pair variant (5) for
+        // codes of check degree 9..20; the default is one row per thread (variant 2), which
+        // measured ~4% faster on C5a (profiles/r1v4_split_ab.md)
+        const char* env = std::getenv("QKD_SPLIT");
+        const bool allow = env && env[0] == '1';
+        c->split = choose_variant(Mb, (int64_t)Nb * Z, (int64_t)Mb * Z, nb, md, di.smem_optin, allow) == 5;
+    }
     c->Mb = Mb;
     c->Nb = Nb;
     c->Z = Z;
@@ -543,7 +637,14 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
             return fail(QKD_EUNSUP, "check degree > 64 in block row " + std::to_string(I));
         }
         c->maxdeg = std::max(c->maxdeg, li.x);
-        li.w = (li.x + 3) & ~3;
+        if (c->split) {   // side A words [0, WA), side B words [WA, WA + roundup2(HB))
+            const int ha = li.x >> 1, hb = li.x - ha;
+            li.w = ((ha + 1) & ~1) + ((hb + 1) & ~1);
+            c->soff.push_back(c->nsplit);
+            c->nsplit += 2 * hb;
+        } else {
+            li.w = (li.x + 3) & ~3;
+        }
         li.z = (int)c->ws_words;
         c->ws_words += (int64_t)Z * li.w;
         if (c->ws_words > (1LL << 31) - 1) {
@@ -560,6 +661,11 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
     if (e == cudaSuccess) e = cudaMemcpy(c->d_layer, c->layer.data(), sizeof(int4) * c->layer.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !c->edge.empty())
         e = cudaMemcpy(c->d_edge, c->edge.data(), sizeof(int2) * c->edge.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && c->split) {
+        e = cudaMalloc(&c->d_soff, sizeof(int) * c->soff.size());
+        if (e == cudaSuccess)
+            e = cudaMemcpy(c->d_soff, c->soff.data(), sizeof(int) * c->soff.size(), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess && pos_kind) {
         bool any = false;
         std::vector<uint8_t> pay((size_t)(c->n + 7) / 8, 0);
@@ -594,6 +700,7 @@ void qkd_code_destroy(qkd_code* c) {
     if (c->d_edge) cudaFree(c->d_edge);
     if (c->d_kind) cudaFree(c->d_kind);
     if (c->d_payload) cudaFree(c->d_payload);
+    if (c->d_soff) cudaFree(c->d_soff);
     delete c;
 }
 
@@ -682,6 +789,8 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
     DecParams p{};
     p.layer = c->d_layer;
     p.edge = c->d_edge;
+    p.soff = c->split ? c->d_soff : nullptr;
+    p.nsplit = c->nsplit;
     p.Mb = c->Mb;
     p.Z = c->Z;
     p.nbase = c->nbase;

@@ -17,7 +17,7 @@ namespace qkd {
 // to the compiler); in_regs() pins them in ordinary registers so ptxas neither folds them nor
 // re-materialises them per use.
 struct Konst {
-    uint32_t one, two, m1, m2, m256, b128, c63, c127;
+    uint32_t one, two, m1, m2, m256, b128, c63, c127, sh26;
     __device__ __forceinline__ Konst in_regs() const {
         Konst k;
         asm volatile("mov.b32 %0, %1;" : "=r"(k.one) : "r"(one));
@@ -28,6 +28,7 @@ struct Konst {
         asm volatile("mov.b32 %0, %1;" : "=r"(k.b128) : "r"(b128));
         asm volatile("mov.b32 %0, %1;" : "=r"(k.c63) : "r"(c63));
         asm volatile("mov.b32 %0, %1;" : "=r"(k.c127) : "r"(c127));
+        k.sh26 = sh26;   // only ever a multiplier: may stay a uniform / constant operand
         return k;
     }
 };
@@ -83,6 +84,27 @@ __device__ __forceinline__ uint32_t tau4(uint32_t a, uint32_t b, const Konst& K)
     const uint32_t g2 = lop3<0xF4>(t2, t1, P);                   // t2 | (t1 & ~P): ... l<=2
     const uint32_t c = imad(g1, K.one, g2) >> 6;
     return imad(c, K.m1, l);
+}
+
+// The same Algorithm 1 in complement form: a' = 63 - a, b' = 63 - b in, 63 - tau(a, b) out.
+// Then g = max(a', b') = 63 - l = (a' + b' + d) / 2 is one IADD3 + SHF, and 63 - tau = g + c is one
+// LEA.HI of the flag word (c = (g1 + g2) >> 6), two instructions fewer than tau4.
+//   l <= 2  <=>  g >= 61  (bit 6 of g + 3);   l == 0  <=>  g == 63  (bit 6 of g + 1)
+//   c = [l>=3]([d<2] + [d<6]) + [1<=l<=2][d<4]  as above.
+__device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K) {
+    const uint32_t d = __vabsdiffu4(a, b);                       // ALU
+    const uint32_t g = (a + b + d) >> 1;                         // IADD3 + SHF (a+b+d = 2 max <= 126)
+    const uint32_t p = imad(g, K.one, 0x03030303u);              // bit6: l <= 2
+    const uint32_t z = imad(g, K.one, 0x01010101u);              // bit6: l == 0
+    const uint32_t U = imad(d, K.one, 0x3E3E3E3Eu);              // bit6: d >= 2
+    const uint32_t W = imad(d, K.one, 0x3C3C3C3Cu);              // bit6: d >= 4
+    const uint32_t V = imad(d, K.one, 0x3A3A3A3Au);              // bit6: d >= 6
+    const uint32_t g1 = lop3i<0x02, 0x40404040u>(p, U);          // ~p & ~U & M: l>=3, d<2
+    const uint32_t A = lop3i<0x02, 0x40404040u>(z, W);           // ~z & ~W & M: l>=1, d<4
+    const uint32_t t2 = lop3i<0x02, 0x40404040u>(p, V);          // ~p & ~V & M: l>=3, d<6
+    const uint32_t g2 = lop3<0xF8>(t2, p, A);                    // t2 | (p & A)
+    const uint32_t y = imad(g1, K.one, g2);                      // 64 c per byte (g1 => g2: <= 0x80)
+    return g + (y >> 6);                                         // LEA.HI: 63 - (l - c)
 }
 
 // sign-extend bytes {1,3} into 16-bit lanes / zero-extend bytes {1,3}

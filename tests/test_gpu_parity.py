@@ -177,3 +177,31 @@ def test_full_size_sampled(gpu, name):
     s_bits = oc.syndrome(r["bits"][sl])
     ok = r["success"][sl] == 1
     assert np.array_equal(s_bits[ok], syn.cpu().numpy()[sl][ok])
+
+
+@pytest.mark.parametrize("case", ["deg9to20", "Z96_multiwarp"])
+@pytest.mark.parametrize("F", [1, 7])
+def test_split_variant_parity_edge_cases(gpu, monkeypatch, case, F):
+    """The lane-pair kernel (variant 5, QKD_SPLIT=1 at code creation): same bits, iterations and
+    final L/E as the oracle, including odd degrees (side A's empty slot) and Z % 16 != 0."""
+    monkeypatch.setenv("QKD_SPLIT", "1")
+    shifts, Z = TINY[case]
+    shifts = np.asarray(shifts, dtype=np.int32)
+    Mb, Nb = shifts.shape
+    n, m = Nb * Z, Mb * Z
+    rng = np.random.default_rng(zlib.crc32(f"split/{case}/{F}".encode()))
+    llr = rng.integers(-127, 128, size=(F, n)).astype(np.int8)
+    syn = rng.integers(0, 256, size=(F, (m + 7) // 8), dtype=np.uint8)
+    for T, es in ((0, 1), (1, 0), (9, 1)):
+        g, code = gpu_decode(gpu, shifts, Z, None, llr, syn, T, es)
+        assert code.launch_info(F)["variant"] % 10 == 5
+        assert_same(g, oracle_decode(shifts, Z, llr, syn, T, es))
+
+
+@pytest.mark.parametrize("name,F", [("C3", 12), ("C5a", 9)])
+def test_split_variant_parity_workloads(gpu, monkeypatch, name, F):
+    monkeypatch.setenv("QKD_SPLIT", "1")
+    w, shifts, kind, x, y, llr, syn = workload_inputs(name, F)
+    g, code = gpu_decode(gpu, shifts, w.Z, kind, llr, syn, w.max_iter, w.early_stop)
+    assert code.launch_info(F)["variant"] == 15
+    assert_same(g, oracle_decode(shifts, w.Z, llr, syn, w.max_iter, w.early_stop))
