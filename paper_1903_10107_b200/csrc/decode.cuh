@@ -3,24 +3,16 @@
 //
 // Storage forms:
 //   E word (shared memory, or global for very long frames): byte f = E_j(frame f) + 127
-//   S word (global workspace):                               byte f = 64 - L_ij(frame f)
-// so that X = x + 191 = E'' + S (Eq.(8): x = L_ji = E_j' - L_ij^{t-1}, exact, in [-190, 190])
-// is a sum of non-negative 16-bit lanes and can be formed on the FMA pipe.
+//   T word (global workspace):                               byte f = 192 + L_ij(frame f)
+// so that X = x + 191 = E'' + 256 - T (Eq.(8): x = L_ji = E_j' - L_ij^{t-1}, exact, in
+// [-190, 190]) is a sum of non-negative 16-bit lanes, and the check node's output byte
+// T = 192 + L_new is stored as computed.
 //
 // Workspace layout: per slot, per block row I, row r owns Dp = roundup4(deg_I) consecutive
 // words (edge k of the row at word k), so a row's messages move with 128-bit loads/stores.
 #pragma once
 #include "swar.cuh"
 
-#ifndef QKD_SPLIT_REMAG
-#define QKD_SPLIT_REMAG 0
-#endif
-#ifndef QKD_TAUC
-#define QKD_TAUC 1
-#endif
-#ifndef QKD_SPLIT_KREG
-#define QKD_SPLIT_KREG 1
-#endif
 
 namespace qkd {
 
@@ -83,10 +75,14 @@ struct EdgeIn {
     uint32_t xlo, xhi, cw;
 };
 
-__device__ __forceinline__ EdgeIn edge_in(uint32_t e, uint32_t s, const Konst& K) {
+// e: E word (E + 127 per byte), tw: T word of the old message (192 + L_old per byte).
+// Per byte X = e + (256 - T); as words e + sum_i (256 - T_i) 256^i = e - T + 0x01010100 (mod 2^32).
+__device__ __forceinline__ EdgeIn edge_in(uint32_t e, uint32_t tw, const Konst& K) {
     EdgeIn r;
-    r.xhi = imad(hi16z(e), K.one, hi16z(s));              // lanes {1,3}: e + s
-    r.xlo = imad(r.xhi, K.m256, imad(e, K.one, s));       // lanes {0,2}: (e + s) - 256 * xhi
+    // lanes {1,3}: e + 256 - T.  prmt(e, one) = hi16z(e) with byte 0 of K.one (0x01) in bytes 1, 3,
+    // i.e. + 0x01000100, so the subtraction stays one IMAD (FMA pipe)
+    r.xhi = imad(hi16z(tw), K.m1, prmt<0x4341u>(e, K.one));
+    r.xlo = imad(r.xhi, K.m256, e - tw + 0x01010100u);    // lanes {0,2}: (e + S) - 256 * xhi
     const uint32_t clo = relu_min(r.xlo, K.b128, 0x007E007Eu);   // clamp(X - 128, 0, 126)
     const uint32_t chi = relu_min(r.xhi, K.b128, 0x007E007Eu);
     r.cw = pack16(clo, chi);          // bytes in [0, 126]; bit 6 = (x >= 1) -- x = 0 counts as
@@ -104,18 +100,18 @@ __device__ __forceinline__ uint32_t edge_magc(uint32_t cw, const Konst& K) {
 // merge it with edge_magc, so the split kernel recomputes it instead of keeping it live.
 __device__ __forceinline__ uint32_t edge_magc_alt(uint32_t cw) { return 0x3F3F3F3Fu - __vabsdiffu4(cw, 0x3F3F3F3Fu); }
 
-// Emit for the split kernel, from the pre-layer E word ew and the old message word s_old only
+// Emit for the split kernel, from the pre-layer E word ew and the old message word t_old only
 // (no 16-bit X words kept from edge_in): with oc = 63 - o and M = 0xFF where L_new < 0,
-//   S_new = 64 - L_new = (oc ^ (M & 0x7F)) + [L_new >= 0]          (127 - oc or oc + 1)
-//   E_new'' = clamp(ew + S_old - S_new, 0, 254) = clamp(E + L_new - L_old, -127, 127) + 127,
-// with d = S_old - S_new + 128 in [2, 254] per byte and the sum in 16-bit lanes; Algorithm 2
-// keeps ew where |E| = 127.  Returns S_new.
-__device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t negf, uint32_t s_old, uint32_t ew,
+//   T_new = 192 + L_new = ~(oc ^ (M & 0x7F)) + [L_new < 0]         (129 + oc or 255 - oc)
+//   E_new'' = clamp(ew + T_new - T_old, 0, 254) = clamp(E + L_new - L_old, -127, 127) + 127,
+// with d = T_new - T_old + 128 in [2, 254] per byte and the sum in 16-bit lanes; Algorithm 2
+// keeps ew where |E| = 127.  Returns T_new.
+__device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t negf, uint32_t t_old, uint32_t ew,
                                                const Konst& K, uint32_t& e_out) {
     const uint32_t M = bmask7(imad(negf, K.two, 0u));             // 0xFF where L_new < 0
-    const uint32_t x1 = lop3i<0x78, 0x7F7F7F7Fu>(oc, M);          // oc ^ (M & 0x7F)
-    const uint32_t sn = imad(lop3i<0x0A, 0x01010101u>(M, 0u), K.one, x1);   // + (~M & 1)
-    const uint32_t d = s_old + 0x80808080u - sn;                  // IADD3, exact per byte
+    const uint32_t nx = lop3i<0x87, 0x7F7F7F7Fu>(oc, M);          // ~(oc ^ (M & 0x7F))
+    const uint32_t sn = imad(lop3i<0xA0, 0x01010101u>(M, 0u), K.one, nx);   // + (M & 1)
+    const uint32_t d = sn - t_old + 0x80808080u;                  // IADD3, exact per byte
     const uint32_t hi = imad(hi16z(ew), K.one, hi16z(d));         // lanes {1,3}: ew + d
     const uint32_t lo = imad(hi, K.m256, imad(ew, K.one, d));     // lanes {0,2}
     const uint32_t enew = pack16(relu_min(lo, K.b128, 0x00FE00FEu), relu_min(hi, K.b128, 0x00FE00FEu));
@@ -138,7 +134,7 @@ __device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t negf, const Ed
     const uint32_t enew = pack16(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu));
     const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);                              // G ? ew : enew
-    return imad(Tb, K.m1, 0x01010100u);                           // 128 - T = 64 - L_new
+    return Tb;                                                    // 192 + L_new (stored as is)
 }
 
 // edge_out with the leave-one-out magnitude in complement form oc = 63 - o (tau4c output):
@@ -148,12 +144,12 @@ __device__ __forceinline__ uint32_t edge_out_c(uint32_t oc, uint32_t negf, const
     const uint32_t M = bmask7(imad(negf, K.two, 0u));             // 0xFF where L_new < 0
     const uint32_t om = lop3i<0x48, 0x3F3F3F3Fu>(oc, M);          // (oc ^ 63) & M = o & M
     const uint32_t Tb = imad(om, K.m2, imad(oc, K.m1, 0xFFFFFFFFu));   // 255 - oc - 2 om = 192 + L_new
-    const uint32_t thi = hi16s(Tb);
-    const uint32_t tlo = imad(imad(thi, K.m256, Tb), K.one, 0xFFFFFF00u);
+    const uint32_t thi = hi16s(Tb);                               // lanes {1,3}: L_new - 64
+    const uint32_t tlo = lo16s(Tb);                               // lanes {0,2}: L_new - 64
     const uint32_t enew = pack16(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu));
     const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);
-    return imad(Tb, K.m1, 0x01010100u);                           // 64 - L_new
+    return Tb;                                                    // 192 + L_new
 }
 
 __device__ __forceinline__ uint4 ld4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
@@ -175,7 +171,7 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
     EdgeIn in[D];
     uint32_t P = 0;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) S[v] = first ? make_uint4(0x40404040u, 0x40404040u, 0x40404040u, 0x40404040u)
+    for (int v = 0; v < NV; ++v) S[v] = first ? make_uint4(0xC0C0C0C0u, 0xC0C0C0C0u, 0xC0C0C0C0u, 0xC0C0C0C0u)
                                               : ld4(Lrow + 4 * v);
 #pragma unroll
     for (int k = 0; k < D; ++k) addr[k] = Addr<POW2>::at(et[k], r4, zm4, Z, K);
@@ -212,24 +208,14 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         }
         const uint32_t ew = ldE<ESM>(Eb, a);
         uint32_t eo;
-#if QKD_TAUC
         w4(S[k >> 2], k & 3) = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
-#else
-        w4(S[k >> 2], k & 3) = edge_out(o, Q ^ in[k].cw, in[k], ew, K, eo);
-#endif
         stE<ESM>(Eb, a, eo);
         if (D <= 2 ? (k == 0) : last_of_group(k)) st4(Lrow + (k & ~3), S[k >> 2]);
     };
-#if QKD_TAUC
-    // complement form (tau4c / edge_magc / edge_out_c): two instructions fewer per tau
+    // magnitudes in complement form (tau4c / edge_magc / edge_out_c): two instructions fewer per tau
 #define QKD_TAU tau4c
 #define QKD_MAG edge_magc
 #define QKD_O63 0u
-#else
-#define QKD_TAU tau4
-#define QKD_MAG edge_mag
-#define QKD_O63 0x3F3F3F3Fu
-#endif
     if constexpr (D == 1) {
         emit(0, QKD_O63);                           // empty box-plus -> MSG_max (R6)
     } else if constexpr (D == 2) {
@@ -293,7 +279,7 @@ __device__ __forceinline__ void row_update_split(const int2* __restrict__ et2, i
     uint2 S[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-        if (first || !act || 2 * w >= n) S[w] = make_uint2(0x40404040u, 0x40404040u);
+        if (first || !act || 2 * w >= n) S[w] = make_uint2(0xC0C0C0C0u, 0xC0C0C0C0u);   // L = 0
         else S[w] = *reinterpret_cast<const uint2*>(Lh + 2 * w);
     }
     auto sw = [&](int j) -> uint32_t& { return (j & 1) ? S[j >> 1].y : S[j >> 1].x; };
@@ -372,7 +358,7 @@ __device__ __noinline__ void row_update_generic(const int2* __restrict__ et, int
     uint32_t P = 0;
     for (int k = 0; k < D; ++k) {
         addr[k] = Addr<false>::at(et[k], r4, 0u, Z, K);
-        S[k] = first ? 0x40404040u : Lrow[k];
+        S[k] = first ? 0xC0C0C0C0u : Lrow[k];
         in[k] = edge_in(ldE<ESM>(Eb, addr[k]), S[k], K);
         P ^= in[k].cw;
     }

@@ -202,7 +202,7 @@ __device__ void finalize(const DecParams& p, const int4* s_layer, const uint32_t
                         wk = k < ha ? k : ((ha + 1) & ~1) + (li.x - 1 - k);
                     }
                     lrow[e] = first ? (int8_t)0
-                                    : (int8_t)(64 - (int)((Lslot[li.z + r * li.w + wk] >> (8 * f)) & 0xFFu));
+                                    : (int8_t)((int)((Lslot[li.z + r * li.w + wk] >> (8 * f)) & 0xFFu) - 192);
                 }
             }
         }
@@ -223,7 +223,7 @@ template <int DMAX, bool ESM, bool POW2, bool SPLIT>
 __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1)
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const Konst K = (SPLIT && !QKD_SPLIT_KREG) ? p.K : p.K.in_regs();
+    const Konst K = p.K.in_regs();
     // tables: layer info, then one edge table per slot with the slot's E base folded in
     int4* s_layer = reinterpret_cast<int4*>(smem + p.tab_off);
     int2* s_edges = reinterpret_cast<int2*>(s_layer + p.Mb);
@@ -514,7 +514,7 @@ const void* kernel_of(int variant, bool pow2) {
 
 // 1, 2, -1, -2, -256 as kernel arguments: opaque to ptxas, so a*one + c stays an IMAD (FMA pipe)
 Konst runtime_konst() {
-    return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu, 1u << 26};
+    return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu};
 }
 
 // Decode variant of a code on a device (fixed at code creation: the split variant has its own

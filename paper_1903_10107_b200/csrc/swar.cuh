@@ -10,6 +10,7 @@
 #pragma once
 #include <cstdint>
 
+
 namespace qkd {
 
 // runtime constants 1, 2, -1, -2, -256, the lane bias -128|-128 and the byte constants
@@ -17,7 +18,7 @@ namespace qkd {
 // to the compiler); in_regs() pins them in ordinary registers so ptxas neither folds them nor
 // re-materialises them per use.
 struct Konst {
-    uint32_t one, two, m1, m2, m256, b128, c63, c127, sh26;
+    uint32_t one, two, m1, m2, m256, b128, c63, c127;
     __device__ __forceinline__ Konst in_regs() const {
         Konst k;
         asm volatile("mov.b32 %0, %1;" : "=r"(k.one) : "r"(one));
@@ -28,7 +29,6 @@ struct Konst {
         asm volatile("mov.b32 %0, %1;" : "=r"(k.b128) : "r"(b128));
         asm volatile("mov.b32 %0, %1;" : "=r"(k.c63) : "r"(c63));
         asm volatile("mov.b32 %0, %1;" : "=r"(k.c127) : "r"(c127));
-        k.sh26 = sh26;   // only ever a multiplier: may stay a uniform / constant operand
         return k;
     }
 };
@@ -110,6 +110,8 @@ __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K
 // sign-extend bytes {1,3} into 16-bit lanes / zero-extend bytes {1,3}
 __device__ __forceinline__ uint32_t hi16s(uint32_t w) { return prmt<0xB391u>(w, 0u); }
 __device__ __forceinline__ uint32_t hi16z(uint32_t w) { return prmt<0x4341u>(w, 0u); }
+// sign-extend bytes {0,2} into 16-bit lanes
+__device__ __forceinline__ uint32_t lo16s(uint32_t w) { return prmt<0xA280u>(w, 0u); }
 // pack the low bytes of two 16x2 words back into frame order {0,1,2,3}
 __device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi) { return prmt<0x6240u>(lo, hi); }
 // byte mask 0xFF where bit 7 of the byte is set
