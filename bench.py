@@ -167,7 +167,7 @@ def default_sample(names, cores):
         edges_iter = w.max_iter * (w.shifts() >= 0).sum() * w.Z       # worst-case work per frame
         # ~3e7 scalar edge updates per second per core for the plain -O2 oracle
         per_frame_s = edges_iter / 3e7
-        per[name] = int(max(cores, min(w.frames, cores * max(1, round(4.0 / per_frame_s)))))
+        per[name] = int(max(cores, min(w.frames, cores * max(1, round(12.0 / per_frame_s)))))
     return per
 
 

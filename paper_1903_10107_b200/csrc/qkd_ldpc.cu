@@ -12,6 +12,10 @@
 #include <vector>
 
 #include "decode.cuh"
+
+#ifndef QKD_KEEP_ADDR
+#define QKD_KEEP_ADDR 10   // rows of degree <= this keep their E addresses in registers
+#endif
 #include "qkd_ldpc.h"
 
 using namespace qkd;
@@ -99,7 +103,7 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
     case DD:                                                                                             \
         if constexpr (DD <= DMAX) {                                                                      \
             for (int r = t; r < p.Z; r += p.TG)                                                          \
-                row_update<DD, ESM, POW2, (DMAX <= 8 ? 4 : 10)>(et, p.Z, 4u * r, zm4, Eb, Lslot + li.z + r * li.w, synI[r], first, K); \
+                row_update<DD, ESM, POW2, (DMAX <= 8 ? 4 : QKD_KEEP_ADDR)>(et, p.Z, 4u * r, zm4, Eb, Lslot + li.z + r * li.w, synI[r], first, K); \
             return;                                                                                      \
         }                                                                                                \
         break;
