@@ -139,9 +139,38 @@ int qkd_reconcile_host(const qkd_code* code, double qber, int64_t n_frames,
                        void* device_buffer, size_t device_buffer_bytes, uint8_t* bits_host,
                        int32_t* iters_host, uint8_t* success_host, void* stream);
 
+/* Interactive rate-adaptive reconciliation ("the shortened bits are
+ * selected in turn from the puncturing bits when addition information revealing is
+ * necessary", "multi-interaction is an essential step"; SPEC bob_attempt /
+ * alice_reveal; reading R25 of DESIGN.md).
+ *   order_dev  int32 [d]: the reserved positions in reveal order (DESIGN R19: column weight
+ *              ascending, seeded ties).  Round k (k = 0..max_rounds) treats order[0, s_k) as
+ *              shortened (known, LLR +-127 from alice_bits) and order[s_k, d) as punctured
+ *              (LLR 0), s_k = min(s0 + k * delta, d); every other position is payload.
+ *   Round 0 decodes all frames; round k > 0 re-decodes, from a fresh state, only the frames
+ *   that have not matched their syndrome yet (gathered into a compact batch); the rounds
+ *   stop early when every frame matched or nothing is left to reveal.
+ *   Per frame outputs: bits/iters/success of the round at which it matched (else of the last
+ *   round it ran), rounds_dev = that round index k.  Leakage of a frame that stopped at
+ *   round k: m - (d - s_k) syndrome-and-reveal bits (host side: R20 with p = d - s_k).
+ *   bob_bits_dev, alice_bits_dev [F][ceil(n/8)], syndrome_dev [F][ceil(m/8)] are read only.
+ *   work_dev: qkd_adaptive_work_bytes(code, F) bytes.  The code handle's own pos_kind is
+ *   ignored (the rounds set the pattern).  Synchronises `stream` once per round (the batch
+ *   of still-failed frames is compacted on the host).
+ * Errors: QKD_EINVAL (d < 0, s0 outside [0, d], delta < 1, max_rounds < 0, NULL), QKD_EDIM
+ * (work buffer too small), QKD_ECUDA. */
+size_t qkd_adaptive_work_bytes(const qkd_code* code, int64_t n_frames);
+int qkd_reconcile_adaptive(const qkd_code* code, double qber, int64_t n_frames,
+                           const int32_t* order_dev, int64_t d, int64_t s0, int64_t delta,
+                           int32_t max_rounds, const uint8_t* bob_bits_dev, const uint8_t* alice_bits_dev,
+                           const uint8_t* syndrome_dev, int32_t max_iter, void* work_dev,
+                           size_t work_bytes, uint8_t* bits_dev, int32_t* iters_dev,
+                           int32_t* rounds_dev, uint8_t* success_dev, void* stream);
+
 /* Launch geometry chosen for (code, F) on the current device:
  * info[0] kernel variant (1: degree<=8 smem, 2: degree<=20 smem, 3: generic smem,
- * 4: generic with E in global memory), [1] threads per frame group, [2] frame groups per
+ * 4: generic with E in global memory, 5: degree 9..20 lane-pair rows (QKD_SPLIT=1 at
+ * code creation); +10 when Z is a power of two), [1] threads per frame group, [2] frame groups per
  * CTA, [3] grid, [4] dynamic shared bytes per CTA, [5] frames per group (4), [6] groups. */
 int qkd_launch_info(const qkd_code* code, int64_t n_frames, int32_t* info);
 

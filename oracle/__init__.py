@@ -163,3 +163,67 @@ class Code:
             L.orc_decode_batch(self._h, F, _p(llr), _p(syn), max_iter, early_stop, _p(bits), _p(iters),
                                _p(succ), _p(Lo), _p(Eo), min(nthreads, max(F, 1)))
         return dict(bits=bits, iters=iters, success=succ, L=Lo, E=Eo)
+
+
+# ---------------------------------------------------------------------------------------
+# Interactive rate-adaptive reconciliation (R25), step by step.
+# ---------------------------------------------------------------------------------------
+def reveal_pattern(n: int, order: np.ndarray, s: int) -> np.ndarray:
+    """pos_kind after revealing: order[:s] shortened (2), order[s:] punctured (1), rest payload (0).
+    P:157 "the shortened bits are selected in turn from the puncturing bits"."""
+    kind = np.zeros(n, dtype=np.uint8)
+    order = np.asarray(order, dtype=np.int64)
+    kind[order[s:]] = 1
+    kind[order[:s]] = 2
+    return kind
+
+
+def reveal_rounds(code: "Code", qber: float, y: np.ndarray, x: np.ndarray, syn: np.ndarray, order: np.ndarray,
+                  s0: int, delta: int, max_rounds: int, max_iter: int, nthreads: int | None = None) -> dict:
+    """Bob decodes every frame with s0 shortened positions (SPEC bob_attempt); each frame
+    that fails asks Alice to reveal the next `delta` punctured positions in reveal order (SPEC
+    alice_reveal) and decodes again from scratch, until it matches its syndrome, the
+    punctured positions run out, or max_rounds reveals were made ("multi-interaction").
+    Returns per frame: bits, iters, success of the round it stopped at, rounds = that round index.
+    Frames are independent: a plain loop over rounds, each decoding the frames still failing."""
+    F = y.shape[0]
+    d = len(order)
+    nb8 = (code.n + 7) // 8
+    out = dict(bits=np.zeros((F, nb8), np.uint8), iters=np.zeros(F, np.int32), rounds=np.zeros(F, np.int32),
+               success=np.zeros(F, np.uint8))
+    active = list(range(F))
+    s_prev = -1
+    for k in range(max_rounds + 1):
+        if not active:
+            break
+        s = min(s0 + k * delta, d)
+        if s == s_prev:
+            break
+        s_prev = s
+        last = k == max_rounds or s == d
+        kind = reveal_pattern(code.n, order, s)
+        a = np.array(active)
+        llr = code.build_llr(qber, y[a], kind, x[a])
+        r = code.decode(llr, syn[a], max_iter, 1, want_state=False, nthreads=nthreads)
+        still = []
+        for i, f in enumerate(active):
+            if r["success"][i] or last:
+                out["bits"][f] = r["bits"][i]
+                out["iters"][f] = r["iters"][i]
+                out["success"][f] = r["success"][i]
+                out["rounds"][f] = k
+            if not r["success"][i]:
+                still.append(f)
+        if last:
+            break
+        active = still
+    return out
+
+
+def adaptive_efficiency(m: int, n: int, d: int, s0: int, delta: int, rounds: np.ndarray, qber: float) -> np.ndarray:
+    """Per-frame efficiency after `rounds` reveals: R20 with p = d - s_k, s = s_k, i.e.
+    f = (m - d + s_k) / ((n - d) h2(q)); each reveal round raises the leak by delta bits (SPEC
+    alice_reveal: "leaked_bits increases by exactly k")."""
+    s_k = np.minimum(s0 + np.asarray(rounds, dtype=np.int64) * delta, d)
+    h2 = -qber * np.log2(qber) - (1 - qber) * np.log2(1 - qber)
+    return (m - d + s_k) / ((n - d) * h2)

@@ -51,6 +51,10 @@ def lib():
         L.qkd_reconcile_host.argtypes = [vp, dbl, i64, vp, vp, vp, i32, i32, vp, ctypes.c_size_t, vp, vp,
                                          vp, vp]
         L.qkd_launch_info.argtypes = [vp, i64, vp]
+        L.qkd_adaptive_work_bytes.argtypes = [vp, i64]
+        L.qkd_adaptive_work_bytes.restype = ctypes.c_size_t
+        L.qkd_reconcile_adaptive.argtypes = [vp, dbl, i64, vp, i64, i64, i64, i32, vp, vp, vp, i32, vp,
+                                             ctypes.c_size_t, vp, vp, vp, vp, vp]
         L.qkd_tau_table.argtypes = [vp, vp]
         L.qkd_last_error.argtypes = []
         L.qkd_last_error.restype = ctypes.c_char_p
@@ -204,6 +208,34 @@ class QCCode:
         if want_state:
             r["L"], r["E"] = Lo, Eo
         return r
+
+    # -- interactive rate adaptation (DESIGN R25) ------------------------
+    def reconcile_adaptive(self, qber, order, s0: int, delta: int, max_rounds: int, bob_bits, alice_bits, syn,
+                           max_iter: int, work=None, stream=None):
+        """qkd_reconcile_adaptive: reveal rounds over the reserved positions `order` (int32 cuda).
+        Returns dict(bits, iters, rounds, success) as cuda tensors (the call synchronises once per round)."""
+        torch = _torch()
+        F = bob_bits.shape[0]
+        _need(bob_bits, torch.uint8, (F, self.nb8), "bob_bits")
+        _need(alice_bits, torch.uint8, (F, self.nb8), "alice_bits")
+        _need(syn, torch.uint8, (F, self.mb8), "syn")
+        d = order.numel()
+        _need(order, torch.int32, (d,), "order")
+        dev = bob_bits.device
+        if work is None:
+            nbytes = lib().qkd_adaptive_work_bytes(self._h, F)
+            if nbytes == 0:
+                _check(-4)
+            work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        bits = torch.empty((F, self.nb8), dtype=torch.uint8, device=dev)
+        iters = torch.empty(F, dtype=torch.int32, device=dev)
+        rounds = torch.empty(F, dtype=torch.int32, device=dev)
+        succ = torch.empty(F, dtype=torch.uint8, device=dev)
+        _check(lib().qkd_reconcile_adaptive(self._h, float(qber), F, _ptr(order), d, int(s0), int(delta),
+                                            int(max_rounds), _ptr(bob_bits), _ptr(alice_bits), _ptr(syn),
+                                            int(max_iter), _ptr(work), work.numel(), _ptr(bits), _ptr(iters),
+                                            _ptr(rounds), _ptr(succ), _stream(stream)))
+        return dict(bits=bits, iters=iters, rounds=rounds, success=succ)
 
     # -- harness -----------------------------------------------------------------------
     def score(self, bits, alice_bits, success, counters=None, want_errors=False, stream=None):

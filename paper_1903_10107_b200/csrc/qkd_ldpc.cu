@@ -472,6 +472,52 @@ __global__ void tau_table_kernel(uint8_t* out, Konst K) {
     }
 }
 
+
+// --------------------------------------------------------------------------------------
+// interactive rate adaptation (qkd_reconcile_adaptive): per-round pattern, compaction
+// --------------------------------------------------------------------------------------
+// kind[order[i]] = 2 (shortened) for i < s, 1 (punctured) for s <= i < d; kind is zeroed first
+__global__ void reveal_kind_kernel(const int32_t* __restrict__ order, long long d, long long s, int n,
+                                   uint8_t* __restrict__ kind) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < d; i += (long long)gridDim.x * blockDim.x) {
+        const int j = order[i];
+        if (j >= 0 && j < n) kind[j] = i < s ? 2 : 1;
+    }
+}
+
+// dst row a = src row idx[a] (row_bytes each); one CTA per row, 4-byte moves when aligned
+__global__ void gather_rows_kernel(const int32_t* __restrict__ idx, long long rows, const uint8_t* __restrict__ src,
+                                   int row_bytes, uint8_t* __restrict__ dst) {
+    for (long long a = blockIdx.x; a < rows; a += gridDim.x) {
+        const uint8_t* s = src + (long long)idx[a] * row_bytes;
+        uint8_t* d = dst + a * row_bytes;
+        if ((row_bytes & 3) == 0) {
+            for (int i = threadIdx.x; i < row_bytes / 4; i += blockDim.x)
+                reinterpret_cast<uint32_t*>(d)[i] = reinterpret_cast<const uint32_t*>(s)[i];
+        } else {
+            for (int i = threadIdx.x; i < row_bytes; i += blockDim.x) d[i] = s[i];
+        }
+    }
+}
+
+// results of compacted frame a go to frame idx[a] when it matched (or on the last round)
+__global__ void scatter_results_kernel(const int32_t* __restrict__ idx, long long rows, int nb8, int round,
+                                       int last, const uint8_t* __restrict__ cbits, const int32_t* __restrict__ citers,
+                                       const uint8_t* __restrict__ csucc, uint8_t* __restrict__ bits,
+                                       int32_t* __restrict__ iters, int32_t* __restrict__ rounds,
+                                       uint8_t* __restrict__ success) {
+    for (long long a = blockIdx.x; a < rows; a += gridDim.x) {
+        if (!csucc[a] && !last) continue;
+        const long long f = idx[a];
+        for (int i = threadIdx.x; i < nb8; i += blockDim.x) bits[f * nb8 + i] = cbits[a * nb8 + i];
+        if (threadIdx.x == 0) {
+            iters[f] = citers[a];
+            success[f] = csucc[a];
+            rounds[f] = round;
+        }
+    }
+}
+
 // --------------------------------------------------------------------------------------
 // launch planning
 // --------------------------------------------------------------------------------------
@@ -896,6 +942,84 @@ int qkd_reconcile_host(const qkd_code* c, double qber, int64_t F, const uint8_t*
     QKD_CK(cudaMemcpyAsync(iters_h, d_it, F * 4, cudaMemcpyDeviceToHost, st));
     QKD_CK(cudaMemcpyAsync(succ_h, d_su, F, cudaMemcpyDeviceToHost, st));
     QKD_CK(cudaStreamSynchronize(st));
+    return QKD_OK;
+}
+
+size_t qkd_adaptive_work_bytes(const qkd_code* c, int64_t F) {
+    if (!c || F < 0) return 0;
+    const size_t nb8 = (size_t)((c->n + 7) / 8), mb8 = (size_t)((c->m + 7) / 8), Fs = (size_t)std::max<int64_t>(F, 1);
+    const size_t ws = qkd_workspace_bytes(c, Fs);
+    if (ws == 0) return 0;
+    return align256((size_t)c->n) + align256(Fs * 4) + 3 * align256(Fs * nb8) + align256(Fs * mb8) +
+           align256(Fs * (size_t)c->n) + align256(Fs * 4) + align256(Fs) + align256(ws);
+}
+
+int qkd_reconcile_adaptive(const qkd_code* c, double qber, int64_t F, const int32_t* order, int64_t d, int64_t s0,
+                           int64_t delta, int32_t max_rounds, const uint8_t* bob, const uint8_t* alice,
+                           const uint8_t* syn, int32_t max_iter, void* work, size_t work_bytes, uint8_t* bits,
+                           int32_t* iters, int32_t* rounds, uint8_t* success, void* stream) {
+    if (!c || F < 0 || d < 0 || d > c->n || s0 < 0 || s0 > d || delta < 1 || max_rounds < 0 || max_iter < 0)
+        return fail(QKD_EINVAL, "bad argument");
+    if (F == 0) return QKD_OK;
+    if ((d > 0 && !order) || !bob || !alice || !syn || !work || !bits || !iters || !rounds || !success)
+        return fail(QKD_EINVAL, "null buffer");
+    const int Lq = qkd_llr_magnitude(qber);
+    if (Lq < 0) return Lq;
+    const size_t need = qkd_adaptive_work_bytes(c, F);
+    if (need == 0 || work_bytes < need) return fail(QKD_EDIM, "work buffer too small: need " + std::to_string(need));
+    const int nb8 = (int)((c->n + 7) / 8), mb8 = (int)((c->m + 7) / 8);
+    char* w = static_cast<char*>(work);
+    uint8_t* kind = (uint8_t*)w; w += align256((size_t)c->n);
+    int32_t* idx = (int32_t*)w; w += align256((size_t)F * 4);
+    uint8_t* g_bob = (uint8_t*)w; w += align256((size_t)F * nb8);
+    uint8_t* g_known = (uint8_t*)w; w += align256((size_t)F * nb8);
+    uint8_t* c_bits = (uint8_t*)w; w += align256((size_t)F * nb8);
+    uint8_t* g_syn = (uint8_t*)w; w += align256((size_t)F * mb8);
+    int8_t* llr = (int8_t*)w; w += align256((size_t)F * (size_t)c->n);
+    int32_t* c_iters = (int32_t*)w; w += align256((size_t)F * 4);
+    uint8_t* c_succ = (uint8_t*)w; w += align256((size_t)F);
+    const size_t wsb = qkd_workspace_bytes(c, F);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<int32_t> act((size_t)F);
+    for (int64_t f = 0; f < F; ++f) act[(size_t)f] = (int32_t)f;
+    std::vector<uint8_t> ok;
+    long long s_prev = -1;
+    for (int k = 0; k <= max_rounds && !act.empty(); ++k) {
+        const long long sk = std::min<long long>(s0 + (long long)k * delta, d);
+        if (sk == s_prev) break;                               // nothing left to reveal
+        const bool last = (k == max_rounds) || (sk == d);
+        s_prev = sk;
+        const long long Fa = (long long)act.size();
+        QKD_CK(cudaMemsetAsync(kind, 0, (size_t)c->n, st));
+        if (d > 0) {
+            reveal_kind_kernel<<<(int)std::min<long long>((d + 255) / 256, 148LL * 8), 256, 0, st>>>(order, d, sk,
+                                                                                                   (int)c->n, kind);
+            QKD_CK(cudaGetLastError());
+        }
+        QKD_CK(cudaMemcpyAsync(idx, act.data(), (size_t)Fa * 4, cudaMemcpyHostToDevice, st));
+        const int g = (int)std::min<long long>(Fa, 148LL * 16);
+        gather_rows_kernel<<<g, 256, 0, st>>>(idx, Fa, bob, nb8, g_bob);
+        gather_rows_kernel<<<g, 256, 0, st>>>(idx, Fa, alice, nb8, g_known);
+        gather_rows_kernel<<<g, 256, 0, st>>>(idx, Fa, syn, mb8, g_syn);
+        const long long total = Fa * nb8;
+        build_llr_kernel<<<(int)std::min<long long>((total + 255) / 256, 148LL * 64), 256, 0, st>>>(
+            (int)c->n, nb8, Fa, Lq, g_bob, g_known, kind, llr);
+        QKD_CK(cudaGetLastError());
+        int rc = qkd_decode_batch(c, Fa, llr, g_syn, max_iter, 1, w, wsb, c_bits, c_iters, c_succ, nullptr, nullptr,
+                                  nullptr, stream);
+        if (rc) return rc;
+        scatter_results_kernel<<<g, 256, 0, st>>>(idx, Fa, nb8, k, last ? 1 : 0, c_bits, c_iters, c_succ, bits, iters,
+                                                  rounds, success);
+        QKD_CK(cudaGetLastError());
+        ok.resize((size_t)Fa);
+        QKD_CK(cudaMemcpyAsync(ok.data(), c_succ, (size_t)Fa, cudaMemcpyDeviceToHost, st));
+        QKD_CK(cudaStreamSynchronize(st));
+        std::vector<int32_t> next;
+        for (long long a = 0; a < Fa; ++a)
+            if (!ok[(size_t)a]) next.push_back(act[(size_t)a]);
+        if (last) break;
+        act.swap(next);
+    }
     return QKD_OK;
 }
 

@@ -163,6 +163,12 @@ class Workload:
         kind[order[s:d]] = 1
         return kind
 
+    def reveal_order(self) -> np.ndarray:
+        """int32 [d]: the reserved positions in reveal order (shortened first, then punctured);
+        interactive rounds shorten them in this order (DESIGN R25)."""
+        d, p, s = self.rate_adaptive_counts()
+        return reserved_order(self.shifts(), self.Z, self.order_seed)[:d].astype(np.int32)
+
     def gen(self, f0: int = 0, F: int | None = None, nthreads: int | None = None):
         F = self.frames if F is None else F
         return frames(self.n, self.qber, self.data_seed, f0, F, nthreads)
