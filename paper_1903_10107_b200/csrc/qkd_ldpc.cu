@@ -123,14 +123,19 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
 }
 
 // per-lane syndrome violation mask (bit f set = frame f violates some parity check),
-// group-uniform.  Hard decision bit = (E < 0) = NOT bit 7 of (E'' + 1), E'' = E + 127 (R9).
+// group-uniform, exact for the lanes in `active`.  Hard decision bit = (E < 0) = NOT bit 7 of
+// (E'' + 1), E'' = E + 127 (R9).  A warp whose own rows already show a violation in every
+// active lane stops early: the group's answer for those lanes ("not yet") cannot change.
 template <int DMAX, bool ESM, bool POW2>
 __device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int4* s_layer, const int2* s_edge,
                                                   const unsigned char* Eb, const uint8_t* sSyn, int t,
-                                                  uint32_t* flags, int& chk, int bar, const Konst& K) {
+                                                  uint32_t* flags, int& chk, int bar, const Konst& K,
+                                                  uint32_t active) {
     const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
+    const uint32_t act7 = nib_to_bit7(active);
     uint32_t v = 0;
     for (int I = 0; I < p.Mb; ++I) {
+        if (I > 0 && (__reduce_or_sync(0xffffffffu, v & 0x80808080u) & act7) == act7) break;
         const int4 li = s_layer[I];
         const int2* et = s_edge + li.y;
         const uint8_t* synI = sSyn + I * p.Z;
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 
         uint32_t active = (1u << nl) - 1u;
         int chk = 0;
         if (p.early_stop) {   // iteration-0 check (R10)
-            const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
+            const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
             const uint32_t done = active & ~viol;
             if (done) {
                 finalize(p, s_layer, Eslot, Lslot, f0, done, 0, done, true, t);
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 
                 group_bar(bar, p.TG);
             }
             if (p.early_stop) {
-                const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
+                const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
                 const uint32_t done = active & ~viol;
                 if (done) {
                     finalize(p, s_layer, Eslot, Lslot, f0, done, it, done, false, t);
@@ -357,7 +362,7 @@ __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 
         if (active) {   // ran out of iterations (or early_stop = 0): state after sweep T (R12)
             uint32_t succ = 0;
             if (!p.early_stop)
-                succ = active & ~syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K);
+                succ = active & ~syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
             finalize(p, s_layer, Eslot, Lslot, f0, active, it, succ, it == 0, t);
         }
         group_bar(bar, p.TG);
