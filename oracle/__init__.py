@@ -56,6 +56,13 @@ def _load():
                                        _vp, _vp, _vp, _vp, _vp, ctypes.c_int]
         L.orc_efficiency.argtypes = [ctypes.c_int64] * 4 + [ctypes.c_double]
         L.orc_efficiency.restype = ctypes.c_double
+        for f in ("orc_beta", "orc_beta_eq6"):
+            getattr(L, f).argtypes = [ctypes.c_double, ctypes.c_double]
+            getattr(L, f).restype = ctypes.c_double
+        L.orc_check_node_float.argtypes = [ctypes.c_int, _vp, ctypes.c_int, _vp]
+        L.orc_build_llr_float.argtypes = [ctypes.c_int64, ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp]
+        L.orc_decode_float_batch.argtypes = [_vp, ctypes.c_int64, _vp, _vp, ctypes.c_int, ctypes.c_int,
+                                             _vp, _vp, _vp, _vp, _vp, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -163,6 +170,57 @@ class Code:
             L.orc_decode_batch(self._h, F, _p(llr), _p(syn), max_iter, early_stop, _p(bits), _p(iters),
                                _p(succ), _p(Lo), _p(Eo), min(nthreads, max(F, 1)))
         return dict(bits=bits, iters=iters, success=succ, L=Lo, E=Eo)
+
+
+# ---------------------------------------------------------------------------------------
+# Exact floating-point layered BP (R26), fp64.
+# ---------------------------------------------------------------------------------------
+LLR_KNOWN = 1000.0   # R26: finite stand-in for +-infinity (shortened bits, degree-1 checks)
+
+
+def beta(a: float, b: float) -> float:
+    """Eq.(6) box-plus of two magnitudes, stable form (R26)."""
+    return _load().orc_beta(a, b)
+
+
+def beta_eq6(a: float, b: float) -> float:
+    """Eq.(6) written literally: 2 atanh(tanh(a/2) tanh(b/2))."""
+    return _load().orc_beta_eq6(a, b)
+
+
+def check_node_float(x, s_i: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _load().orc_check_node_float(len(x), _p(x), int(s_i), _p(out))
+    return out
+
+
+def build_llr_float(n: int, qber: float, y_bits: np.ndarray, kind=None, known_bits=None) -> np.ndarray:
+    y = np.ascontiguousarray(y_bits, dtype=np.uint8).reshape(-1, (n + 7) // 8)
+    kd = None if kind is None else np.ascontiguousarray(kind, dtype=np.uint8)
+    kn = None if known_bits is None else np.ascontiguousarray(known_bits, dtype=np.uint8).reshape(y.shape)
+    out = np.empty((y.shape[0], n), dtype=np.float64)
+    for f in range(y.shape[0]):
+        _load().orc_build_llr_float(n, qber, LLR_KNOWN, _p(y[f]), _p(kd), None if kn is None else _p(kn[f]),
+                                    _p(out[f]))
+    return out
+
+
+def decode_float(code: "Code", llr: np.ndarray, syn: np.ndarray, max_iter: int, early_stop: int = 1,
+                 want_state: bool = True, nthreads: int | None = None) -> dict:
+    """Batch fp64 layered BP decode; same outputs as Code.decode with float L and E."""
+    llr = np.ascontiguousarray(llr, dtype=np.float64).reshape(-1, code.n)
+    F = llr.shape[0]
+    syn = np.ascontiguousarray(syn, dtype=np.uint8).reshape(F, (code.m + 7) // 8)
+    bits = np.zeros((F, (code.n + 7) // 8), dtype=np.uint8)
+    iters = np.zeros(F, dtype=np.int32)
+    succ = np.zeros(F, dtype=np.uint8)
+    Lo = np.zeros((F, code.n_edges), dtype=np.float64) if want_state else None
+    Eo = np.zeros((F, code.n), dtype=np.float64) if want_state else None
+    nthreads = nthreads or os.cpu_count() or 1
+    _load().orc_decode_float_batch(code._h, F, _p(llr), _p(syn), max_iter, early_stop, _p(bits), _p(iters),
+                                   _p(succ), _p(Lo), _p(Eo), min(nthreads, max(F, 1)))
+    return dict(bits=bits, iters=iters, success=succ, L=Lo, E=Eo)
 
 
 # ---------------------------------------------------------------------------------------

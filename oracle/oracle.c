@@ -311,3 +311,152 @@ double orc_efficiency(int64_t m, int64_t n, int64_t p, int64_t s, double q) {
     double h = -q * log2(q) - (1.0 - q) * log2(1.0 - q);
     return (double)(m - p) / ((double)(n - p - s) * h);
 }
+
+/* ========================================================================= */
+/* Exact floating-point layered BP, fp64, step by step.    */
+/* The reference the quantized decoder is measured against ("maintain the   */
+/* high efficiency as the floating-point version").                  */
+/* ========================================================================= */
+
+#define ORC_LLR_KNOWN 1000.0   /* R26: stand-in for an infinite LLR (shortened bit, degree-1 check) */
+
+/* Eq.(6): L1 [+] L2 = beta(L1, L2) = 2 atanh(tanh(L1/2) tanh(L2/2)), written literally.  Exact in
+ * exact arithmetic; in fp64 tanh(x/2) rounds to 1 for x > ~38, so the decoder uses orc_beta. */
+double orc_beta_eq6(double a, double b) { return 2.0 * atanh(tanh(a / 2.0) * tanh(b / 2.0)); }
+
+/* The same function for magnitudes a, b >= 0 in its numerically stable textbook form (reading
+ * R26): 2 atanh(tanh(a/2) tanh(b/2)) = min(a,b) + ln(1 + e^{-(a+b)}) - ln(1 + e^{-|a-b|}). */
+double orc_beta(double a, double b) {
+    double m = a < b ? a : b;
+    return m + log1p(exp(-(a + b))) - log1p(exp(-fabs(a - b)));
+}
+
+/* Check node, exact: Eq.(1) sign (syndrome bit folded in, R5), Eq.(2)/(4) magnitude as the box-plus
+ * of the other inputs by the forward/backward schedule of R6 (Eq.(7) nesting; box-plus is
+ * associative, so the schedule only changes rounding).  x: L_ji, out: L_ij. */
+void orc_check_node_float(int d, const double* x, int s_i, double* Lnew) {
+    double mag[256], F[256], B[256];
+    int sg = s_i, neg[256];
+    for (int k = 0; k < d; k++) {
+        neg[k] = x[k] < 0.0;
+        mag[k] = fabs(x[k]);
+        sg ^= neg[k];
+    }
+    double o[256];
+    if (d == 1) {
+        o[0] = ORC_LLR_KNOWN;            /* empty box-plus = +inf, R26's finite stand-in (no inf - inf) */
+    } else {
+        F[0] = mag[0];
+        for (int k = 1; k < d; k++) F[k] = orc_beta(F[k - 1], mag[k]);
+        B[d - 1] = mag[d - 1];
+        for (int k = d - 2; k >= 0; k--) B[k] = orc_beta(mag[k], B[k + 1]);
+        o[0] = B[1];
+        o[d - 1] = F[d - 2];
+        for (int k = 1; k < d - 1; k++) o[k] = orc_beta(F[k - 1], B[k + 1]);
+    }
+    for (int k = 0; k < d; k++) Lnew[k] = (sg ^ neg[k]) ? -o[k] : o[k];
+}
+
+static int syndrome_ok_f(const orc_code* c, const double* E, const uint8_t* syn) {
+    for (int I = 0; I < c->Mb; I++)
+        for (int r = 0; r < c->Z; r++) {
+            int64_t i = (int64_t)I * c->Z + r;
+            int p = (syn[i >> 3] >> (i & 7)) & 1;
+            for (int k = 0; k < c->deg[I]; k++) p ^= E[col_of(c, I, r, k)] < 0.0;   /* bit = (E<0), R9 */
+            if (p) return 0;
+        }
+    return 1;
+}
+
+/* Channel LLR, exact (P:103-104 before quantization): ln((1-q)/q) by Bob's bit; punctured 0;
+ * shortened +-known_llr (reading R26: a finite stand-in for +-infinity). */
+void orc_build_llr_float(int64_t n, double q, double known_llr, const uint8_t* y_bits, const uint8_t* kind,
+                         const uint8_t* known_bits, double* llr) {
+    double Lc = log((1.0 - q) / q);
+    for (int64_t j = 0; j < n; j++) {
+        int yb = (y_bits[j >> 3] >> (j & 7)) & 1;
+        int kd = kind ? kind[j] : 0;
+        if (kd == 1) llr[j] = 0.0;
+        else if (kd == 2) llr[j] = ((known_bits[j >> 3] >> (j & 7)) & 1) ? -known_llr : known_llr;
+        else llr[j] = yb ? -Lc : Lc;
+    }
+}
+
+/* Layered BP decode of one frame (P:91-97 with Eq.(8) L_ji = E_j - L_ij, Eq.(9) E_j = L_ji + L_ij,
+ * no saturation); same schedule, stopping rule and outputs as orc_decode (R10-R13, R16). */
+int orc_decode_float(const orc_code* c, const double* llr, const uint8_t* syn, int T, int early_stop,
+                     uint8_t* bits, int32_t* iters, uint8_t* success, double* L_out, double* E_out) {
+    int64_t n = c->n;
+    double* E = (double*)malloc(sizeof(double) * n);
+    double* L = (double*)calloc((size_t)c->n_edges, sizeof(double));
+    double x[256], Ln[256];
+    int64_t jk[256];
+    for (int64_t j = 0; j < n; j++) E[j] = llr[j];
+    int t_done = 0, ok = 0;
+    if (early_stop && syndrome_ok_f(c, E, syn)) { ok = 1; goto finish; }
+    for (int t = 1; t <= T; t++) {
+        for (int I = 0; I < c->Mb; I++) {
+            int d = c->deg[I];
+            for (int r = 0; r < c->Z; r++) {
+                int64_t i = (int64_t)I * c->Z + r;
+                int s_i = (syn[i >> 3] >> (i & 7)) & 1;
+                for (int k = 0; k < d; k++) {
+                    jk[k] = col_of(c, I, r, k);
+                    x[k] = E[jk[k]] - L[edge_of(c, I, r, k)];        /* Eq.(8) */
+                }
+                orc_check_node_float(d, x, s_i, Ln);
+                for (int k = 0; k < d; k++) {
+                    L[edge_of(c, I, r, k)] = Ln[k];
+                    E[jk[k]] = x[k] + Ln[k];                          /* Eq.(9) */
+                }
+            }
+        }
+        t_done = t;
+        if (early_stop && syndrome_ok_f(c, E, syn)) { ok = 1; goto finish; }
+    }
+    ok = early_stop ? 0 : syndrome_ok_f(c, E, syn);
+finish:
+    memset(bits, 0, (size_t)((n + 7) / 8));
+    for (int64_t j = 0; j < n; j++) if (E[j] < 0.0) bits[j >> 3] |= (uint8_t)(1u << (j & 7));
+    *iters = t_done;
+    *success = (uint8_t)ok;
+    if (L_out) memcpy(L_out, L, sizeof(double) * (size_t)c->n_edges);
+    if (E_out) memcpy(E_out, E, sizeof(double) * (size_t)n);
+    free(E); free(L);
+    return 0;
+}
+
+typedef struct {
+    const orc_code* c; const double* llr; const uint8_t* syn; int T, es;
+    uint8_t* bits; int32_t* iters; uint8_t* succ; double* L; double* E;
+    int64_t F; int64_t next; pthread_mutex_t mu;
+} batch_job_f;
+
+static void* batch_worker_f(void* p) {
+    batch_job_f* b = (batch_job_f*)p;
+    const orc_code* c = b->c;
+    int64_t nb = (c->n + 7) / 8, sb = (c->m + 7) / 8;
+    for (;;) {
+        pthread_mutex_lock(&b->mu);
+        int64_t f = b->next++;
+        pthread_mutex_unlock(&b->mu);
+        if (f >= b->F) break;
+        orc_decode_float(c, b->llr + f * c->n, b->syn + f * sb, b->T, b->es, b->bits + f * nb, b->iters + f,
+                         b->succ + f, b->L ? b->L + f * c->n_edges : NULL, b->E ? b->E + f * c->n : NULL);
+    }
+    return NULL;
+}
+
+int orc_decode_float_batch(const orc_code* c, int64_t F, const double* llr, const uint8_t* syn, int T,
+                           int early_stop, uint8_t* bits, int32_t* iters, uint8_t* success, double* L_out,
+                           double* E_out, int nthreads) {
+    batch_job_f b = { c, llr, syn, T, early_stop, bits, iters, success, L_out, E_out, F, 0 };
+    pthread_mutex_init(&b.mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 512) nthreads = 512;
+    pthread_t th[512];
+    for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, batch_worker_f, &b);
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&b.mu);
+    return 0;
+}
