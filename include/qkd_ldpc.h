@@ -167,6 +167,24 @@ int qkd_reconcile_adaptive(const qkd_code* code, double qber, int64_t n_frames,
                            size_t work_bytes, uint8_t* bits_dev, int32_t* iters_dev,
                            int32_t* rounds_dev, uint8_t* success_dev, void* stream);
 
+/* Exact floating-point layered BP (R26): the reference decoder the
+ * quantized path is compared with ("maintain the high efficiency as the floating-point
+ * version").  Check node Eq.(1) + Eq.(2)/(4) with the box-plus of Eq.(6)/(7) (forward/backward
+ * schedule of R6, beta in R26's stable form), variable node Eq.(8)/(9) without saturation, the
+ * same layered schedule and stopping rule as qkd_decode_batch; fp32 throughout.
+ * qkd_build_llr_float: llr_dev float [F][n] = +-ln((1-q)/q) by Bob's bit, 0 punctured, +-1000 for
+ *   shortened positions (known_bits required when the code has them).
+ * qkd_decode_float_batch: like qkd_decode_batch with float LLRs; final_L_dev (float [F][n_edges],
+ *   canonical order) and final_E_dev (float [F][n]) optional.  Check degrees <= 20.
+ * Errors: QKD_EINVAL, QKD_EDIM (workspace too small), QKD_EUNSUP (degree > 20), QKD_ECUDA. */
+int qkd_build_llr_float(const qkd_code* code, double qber, int64_t n_frames, const uint8_t* bob_bits_dev,
+                        const uint8_t* known_bits_dev, float* llr_dev, void* stream);
+size_t qkd_float_workspace_bytes(const qkd_code* code, int64_t n_frames);
+int qkd_decode_float_batch(const qkd_code* code, int64_t n_frames, const float* llr_dev,
+                           const uint8_t* syndrome_dev, int32_t max_iter, int32_t early_stop,
+                           void* workspace_dev, size_t workspace_bytes, uint8_t* bits_dev, int32_t* iters_dev,
+                           uint8_t* success_dev, float* final_L_dev, float* final_E_dev, void* stream);
+
 /* Launch geometry chosen for (code, F) on the current device:
  * info[0] kernel variant (1: degree<=8 smem, 2: degree<=20 smem, 3: generic smem,
  * 4: generic with E in global memory, 5: degree 9..20 lane-pair rows (QKD_SPLIT=1 at

@@ -51,6 +51,11 @@ def lib():
         L.qkd_reconcile_host.argtypes = [vp, dbl, i64, vp, vp, vp, i32, i32, vp, ctypes.c_size_t, vp, vp,
                                          vp, vp]
         L.qkd_launch_info.argtypes = [vp, i64, vp]
+        L.qkd_build_llr_float.argtypes = [vp, dbl, i64, vp, vp, vp, vp]
+        L.qkd_float_workspace_bytes.argtypes = [vp, i64]
+        L.qkd_float_workspace_bytes.restype = ctypes.c_size_t
+        L.qkd_decode_float_batch.argtypes = [vp, i64, vp, vp, i32, i32, vp, ctypes.c_size_t, vp, vp, vp, vp, vp,
+                                             vp]
         L.qkd_adaptive_work_bytes.argtypes = [vp, i64]
         L.qkd_adaptive_work_bytes.restype = ctypes.c_size_t
         L.qkd_reconcile_adaptive.argtypes = [vp, dbl, i64, vp, i64, i64, i64, i32, vp, vp, vp, i32, vp,
@@ -204,6 +209,44 @@ class QCCode:
         _check(lib().qkd_decode_batch(self._h, F, _ptr(llr), _ptr(syn), int(max_iter), int(bool(early_stop)),
                                       _ptr(workspace), workspace.numel(), _ptr(bits), _ptr(iters), _ptr(succ),
                                       _ptr(Lo), _ptr(Eo), _ptr(counters), _stream(stream)))
+        r = dict(bits=bits, iters=iters, success=succ)
+        if want_state:
+            r["L"], r["E"] = Lo, Eo
+        return r
+
+    # -- exact floating-point BP (DESIGN R26) ---------------------------
+    def build_llr_float(self, qber, bob_bits, known_bits=None, out=None, stream=None):
+        torch = _torch()
+        F = bob_bits.shape[0]
+        _need(bob_bits, torch.uint8, (F, self.nb8), "bob_bits")
+        if known_bits is not None:
+            _need(known_bits, torch.uint8, (F, self.nb8), "known_bits")
+        out = out if out is not None else torch.empty((F, self.n), dtype=torch.float32, device=bob_bits.device)
+        _check(lib().qkd_build_llr_float(self._h, float(qber), F, _ptr(bob_bits), _ptr(known_bits), _ptr(out),
+                                         _stream(stream)))
+        return out
+
+    def decode_float(self, llr, syn, max_iter: int, early_stop: bool = True, want_state: bool = False,
+                     workspace=None, stream=None):
+        """qkd_decode_float_batch: dict(bits, iters, success[, L, E]) as cuda tensors (asynchronous)."""
+        torch = _torch()
+        F = llr.shape[0]
+        _need(llr, torch.float32, (F, self.n), "llr")
+        _need(syn, torch.uint8, (F, self.mb8), "syn")
+        dev = llr.device
+        bits = torch.empty((F, self.nb8), dtype=torch.uint8, device=dev)
+        iters = torch.empty(F, dtype=torch.int32, device=dev)
+        succ = torch.empty(F, dtype=torch.uint8, device=dev)
+        Lo = torch.empty((F, self.n_edges), dtype=torch.float32, device=dev) if want_state else None
+        Eo = torch.empty((F, self.n), dtype=torch.float32, device=dev) if want_state else None
+        if workspace is None:
+            nbytes = lib().qkd_float_workspace_bytes(self._h, F)
+            if nbytes == 0:
+                _check(-6)
+            workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        _check(lib().qkd_decode_float_batch(self._h, F, _ptr(llr), _ptr(syn), int(max_iter), int(bool(early_stop)),
+                                            _ptr(workspace), workspace.numel(), _ptr(bits), _ptr(iters), _ptr(succ),
+                                            _ptr(Lo), _ptr(Eo), _stream(stream)))
         r = dict(bits=bits, iters=iters, success=succ)
         if want_state:
             r["L"], r["E"] = Lo, Eo

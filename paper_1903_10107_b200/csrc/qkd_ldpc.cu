@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "decode.cuh"
+#include "decode_float.cuh"
 
 #ifndef QKD_KEEP_ADDR
 #define QKD_KEEP_ADDR 10   // rows of degree <= this keep their E addresses in registers
@@ -523,6 +524,117 @@ __global__ void scatter_results_kernel(const int32_t* __restrict__ idx, long lon
     }
 }
 
+
+// --------------------------------------------------------------------------------------
+// exact floating-point layered BP (decode_float.cuh): one frame per slot
+// --------------------------------------------------------------------------------------
+template <bool ESM>
+__global__ void __launch_bounds__(1024, 1) decode_float_kernel(const FParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int4* s_layer = reinterpret_cast<int4*>(smem + p.tab_off);
+    int2* s_edge = reinterpret_cast<int2*>(s_layer + p.Mb);
+    for (int i = threadIdx.x; i < p.Mb; i += blockDim.x) s_layer[i] = p.layer[i];
+    for (int i = threadIdx.x; i < p.nbase; i += blockDim.x) s_edge[i] = p.edge[i];
+    __syncthreads();
+    const int slot = threadIdx.x / p.TG;
+    const int t = threadIdx.x - slot * p.TG;
+    const int bar = 1 + slot;
+    const long long gslot = (long long)blockIdx.x * p.GPC + slot;
+    unsigned char* sbase = smem + (size_t)slot * p.slot_bytes;
+    float* E = ESM ? reinterpret_cast<float*>(sbase) : p.Ews + gslot * (long long)p.n;
+    uint8_t* sSyn = sbase + p.e_bytes;
+    int* ctl = reinterpret_cast<int*>(sSyn + ((p.m + 15) & ~15));
+    float* Ls = p.Lws + gslot * p.ws_words;
+    const int lane = threadIdx.x & 31;
+
+    auto syndrome_ok = [&]() -> bool {   // every check row's parity of (E < 0) equals its target bit
+        int v = 0;
+        for (int I = 0; I < p.Mb; ++I) {
+            const int4 li = s_layer[I];
+            for (int r = t; r < p.Z; r += p.TG) {
+                int par = sSyn[I * p.Z + r];
+                for (int k = 0; k < li.x; ++k) par ^= E[col_f(s_edge[li.y + k], r, p.Z)] < 0.0f;
+                v |= par;
+            }
+        }
+        v = __reduce_or_sync(0xffffffffu, v);
+        if (lane == 0 && v) atomicOr(&ctl[1], 1);
+        group_bar(bar, p.TG);
+        const int res = *(volatile int*)&ctl[1];
+        group_bar(bar, p.TG);
+        if (t == 0) ctl[1] = 0;
+        return res == 0;
+    };
+
+    for (;;) {
+        if (t == 0) { ctl[0] = atomicAdd(p.work, 1); ctl[1] = 0; }
+        group_bar(bar, p.TG);
+        const long long f = *(volatile int*)&ctl[0];
+        if (f >= p.F) break;
+        for (int j = t; j < p.n; j += p.TG) E[j] = p.llr[f * p.n + j];
+        for (int i = t; i < p.m; i += p.TG) sSyn[i] = (p.syn[f * p.mb8 + (i >> 3)] >> (i & 7)) & 1;
+        group_bar(bar, p.TG);
+        int it = 0;
+        bool ok = false;
+        if (p.early_stop) ok = syndrome_ok();   // iteration-0 check (R10)
+        while (!ok && it < p.T) {
+            ++it;
+            for (int I = 0; I < p.Mb; ++I) {
+                const int4 li = s_layer[I];
+                for (int r = t; r < p.Z; r += p.TG)
+                    row_update_f(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
+                                 sSyn[I * p.Z + r], it == 1);
+                group_bar(bar, p.TG);
+            }
+            if (p.early_stop) ok = syndrome_ok();
+        }
+        if (!p.early_stop) ok = syndrome_ok();   // R12
+        // outputs: bits (E < 0, R9), iters, success; optional final L (canonical order) and E
+        uint8_t* brow = p.bits + f * p.nb8;
+        for (int jw = t & ~31; jw < p.n; jw += p.TG) {
+            const int j = jw + lane;
+            const bool b = j < p.n && E[j < p.n ? j : 0] < 0.0f;
+            const uint32_t bal = __ballot_sync(0xffffffffu, b);
+            const int byte = (jw >> 3) + lane;
+            if (lane < 4 && byte < p.nb8) brow[byte] = (uint8_t)(bal >> (8 * lane));
+        }
+        if (p.fE)
+            for (int j = t; j < p.n; j += p.TG) p.fE[f * p.n + j] = E[j];
+        if (p.fL) {
+            for (int I = 0; I < p.Mb; ++I) {
+                const int4 li = s_layer[I];
+                for (int q = t; q < li.x * p.Z; q += p.TG) {
+                    const int k = q / p.Z, r = q - k * p.Z;
+                    p.fL[f * p.n_edges + (long long)(li.y + k) * p.Z + r] =
+                        it == 0 ? 0.0f : Ls[li.z + (long long)r * li.w + k];
+                }
+            }
+        }
+        if (t == 0) {
+            p.iters[f] = it;
+            p.success[f] = ok ? 1 : 0;
+        }
+        group_bar(bar, p.TG);
+    }
+}
+
+__global__ void build_llr_float_kernel(int n, int nb8, long long F, float Lc, const uint8_t* __restrict__ y,
+                                       const uint8_t* __restrict__ known, const uint8_t* __restrict__ kind,
+                                       float* __restrict__ llr) {
+    const long long total = F * (long long)n;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long f = q / n;
+        const int j = (int)(q - f * n);
+        const int kd = kind ? kind[j] : 0;
+        float v;
+        if (kd == 1) v = 0.0f;
+        else if (kd == 2) v = ((known[f * nb8 + (j >> 3)] >> (j & 7)) & 1) ? -kLlrKnown : kLlrKnown;
+        else v = ((y[f * nb8 + (j >> 3)] >> (j & 7)) & 1) ? -Lc : Lc;
+        llr[q] = v;
+    }
+}
+
 // --------------------------------------------------------------------------------------
 // launch planning
 // --------------------------------------------------------------------------------------
@@ -1025,6 +1137,119 @@ int qkd_reconcile_adaptive(const qkd_code* c, double qber, int64_t F, const int3
         if (last) break;
         act.swap(next);
     }
+    return QKD_OK;
+}
+
+// ---- exact floating-point BP ---------------------------------------
+struct FPlan {
+    bool esm = false;
+    int TG = 0, GPC = 0, grid = 0, smem = 0, slot_bytes = 0, e_bytes = 0, tab_off = 0;
+    long long slots = 0;
+    size_t ws_total = 0;
+};
+
+static int make_fplan(const qkd_code* c, long long F, FPlan& pl) {
+    if (c->maxdeg > kFloatDMax) return fail(QKD_EUNSUP, "float decoder: check degree > 20");
+    int dev = 0;
+    QKD_CK(cudaGetDevice(&dev));
+    const DevInfo di = dev_info(dev);
+    if (!di.ok) return fail(QKD_ECUDA, "cannot query device attributes");
+    const long long tab = (long long)c->Mb * sizeof(int4) + (long long)c->nbase * sizeof(int2);
+    const long long syn_ctl = ((c->m + 15) & ~15LL) + 16;
+    pl.esm = 4LL * c->n + syn_ctl + tab <= di.smem_optin;
+    pl.e_bytes = pl.esm ? (int)(4LL * c->n) : 0;
+    pl.slot_bytes = (int)((pl.e_bytes + syn_ctl + 15) & ~15LL);
+    if (pl.slot_bytes + tab > di.smem_optin) return fail(QKD_EUNSUP, "float decoder: frame too long");
+    pl.TG = (int)std::min<long long>(((long long)c->Z + 31) / 32 * 32, 512);
+    int gpc = std::max(1, 1024 / pl.TG);
+    while (gpc > 1 && (long long)gpc * pl.slot_bytes + tab > di.smem_optin) --gpc;
+    gpc = (int)std::max<long long>(1, std::min<long long>(gpc, (F + di.sms - 1) / di.sms));
+    pl.GPC = gpc;
+    pl.tab_off = gpc * pl.slot_bytes;
+    pl.smem = pl.tab_off + (int)tab;
+    const void* k = pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true>)
+                           : reinterpret_cast<const void*>(&decode_float_kernel<false>);
+    QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+    int per_sm = 0;
+    QKD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.TG * pl.GPC, pl.smem));
+    if (per_sm < 1) return fail(QKD_EUNSUP, "float decoder cannot be resident with this geometry");
+    const long long ctas = (F + gpc - 1) / gpc;
+    pl.grid = (int)std::max<long long>(1, std::min<long long>(ctas, (long long)per_sm * di.sms));
+    pl.slots = (long long)pl.grid * gpc;
+    pl.ws_total = 256 + (size_t)pl.slots * (size_t)c->ws_words * 4 + (pl.esm ? 0 : (size_t)pl.slots * c->n * 4);
+    return QKD_OK;
+}
+
+size_t qkd_float_workspace_bytes(const qkd_code* c, int64_t F) {
+    if (!c || F < 0) return 0;
+    FPlan pl;
+    if (make_fplan(c, std::max<int64_t>(F, 1), pl) != QKD_OK) return 0;
+    return pl.ws_total;
+}
+
+int qkd_build_llr_float(const qkd_code* c, double qber, int64_t F, const uint8_t* y, const uint8_t* known,
+                        float* llr, void* stream) {
+    if (!c || F < 0 || (F > 0 && (!y || !llr))) return fail(QKD_EINVAL, "bad argument");
+    if (!(qber > 0.0 && qber < 0.5)) return fail(QKD_EINVAL, "qber must lie in (0, 0.5)");
+    if (c->has_short && !known) return fail(QKD_EINVAL, "code has shortened positions: known_bits required");
+    if (F == 0) return QKD_OK;
+    const float Lc = (float)std::log((1.0 - qber) / qber);
+    const long long total = F * c->n;
+    build_llr_float_kernel<<<(int)std::min<long long>((total + 255) / 256, 148LL * 64), 256, 0, (cudaStream_t)stream>>>(
+        (int)c->n, (int)((c->n + 7) / 8), F, Lc, y, c->d_kind ? known : nullptr, c->d_kind, llr);
+    QKD_CK(cudaGetLastError());
+    return QKD_OK;
+}
+
+int qkd_decode_float_batch(const qkd_code* c, int64_t F, const float* llr, const uint8_t* syn, int32_t max_iter,
+                           int32_t early_stop, void* ws, size_t ws_bytes, uint8_t* bits, int32_t* iters,
+                           uint8_t* success, float* fL, float* fE, void* stream) {
+    if (!c || F < 0 || max_iter < 0) return fail(QKD_EINVAL, "bad argument");
+    if (F == 0) return QKD_OK;
+    if (!llr || !syn || !ws || !bits || !iters || !success) return fail(QKD_EINVAL, "null buffer");
+    FPlan pl;
+    int rc = make_fplan(c, F, pl);
+    if (rc) return rc;
+    if (ws_bytes < pl.ws_total)
+        return fail(QKD_EDIM, "workspace too small: need " + std::to_string(pl.ws_total) + " bytes");
+    char* w = static_cast<char*>(ws);
+    FParams p{};
+    p.layer = c->d_layer;
+    p.edge = c->d_edge;
+    p.Mb = c->Mb;
+    p.Z = c->Z;
+    p.nbase = c->nbase;
+    p.n = (int)c->n;
+    p.m = (int)c->m;
+    p.mb8 = (int)((c->m + 7) / 8);
+    p.nb8 = (int)((c->n + 7) / 8);
+    p.n_edges = c->n_edges;
+    p.ws_words = c->ws_words;
+    p.llr = llr;
+    p.syn = syn;
+    p.F = F;
+    p.T = max_iter;
+    p.early_stop = early_stop ? 1 : 0;
+    p.work = reinterpret_cast<int*>(w);
+    p.Lws = reinterpret_cast<float*>(w + 256);
+    p.Ews = pl.esm ? nullptr : reinterpret_cast<float*>(w + 256 + (size_t)pl.slots * (size_t)c->ws_words * 4);
+    p.bits = bits;
+    p.iters = iters;
+    p.success = success;
+    p.fL = fL;
+    p.fE = fE;
+    p.TG = pl.TG;
+    p.GPC = pl.GPC;
+    p.slot_bytes = pl.slot_bytes;
+    p.e_bytes = pl.e_bytes;
+    p.tab_off = pl.tab_off;
+    cudaStream_t st = (cudaStream_t)stream;
+    QKD_CK(cudaMemsetAsync(p.work, 0, sizeof(int), st));
+    void* args[] = {&p};
+    const void* k = pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true>)
+                           : reinterpret_cast<const void*>(&decode_float_kernel<false>);
+    QKD_CK(cudaLaunchKernel(k, dim3(pl.grid), dim3(pl.TG * pl.GPC), args, pl.smem, st));
+    QKD_CK(cudaGetLastError());
     return QKD_OK;
 }
 
