@@ -62,7 +62,7 @@ def _load():
         L.orc_check_node_float.argtypes = [ctypes.c_int, _vp, ctypes.c_int, _vp]
         L.orc_build_llr_float.argtypes = [ctypes.c_int64, ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp]
         L.orc_decode_float_batch.argtypes = [_vp, ctypes.c_int64, _vp, _vp, ctypes.c_int, ctypes.c_int,
-                                             _vp, _vp, _vp, _vp, _vp, ctypes.c_int]
+                                             _vp, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -207,8 +207,9 @@ def build_llr_float(n: int, qber: float, y_bits: np.ndarray, kind=None, known_bi
 
 
 def decode_float(code: "Code", llr: np.ndarray, syn: np.ndarray, max_iter: int, early_stop: int = 1,
-                 want_state: bool = True, nthreads: int | None = None) -> dict:
-    """Batch fp64 layered BP decode; same outputs as Code.decode with float L and E."""
+                 want_state: bool = True, nthreads: int | None = None, flooding: bool = False) -> dict:
+    """Batch fp64 BP decode (layered, or the flooding schedule of N4); same outputs as Code.decode
+    with float L and E."""
     llr = np.ascontiguousarray(llr, dtype=np.float64).reshape(-1, code.n)
     F = llr.shape[0]
     syn = np.ascontiguousarray(syn, dtype=np.uint8).reshape(F, (code.m + 7) // 8)
@@ -219,7 +220,7 @@ def decode_float(code: "Code", llr: np.ndarray, syn: np.ndarray, max_iter: int, 
     Eo = np.zeros((F, code.n), dtype=np.float64) if want_state else None
     nthreads = nthreads or os.cpu_count() or 1
     _load().orc_decode_float_batch(code._h, F, _p(llr), _p(syn), max_iter, early_stop, _p(bits), _p(iters),
-                                   _p(succ), _p(Lo), _p(Eo), min(nthreads, max(F, 1)))
+                                   _p(succ), _p(Lo), _p(Eo), min(nthreads, max(F, 1)), int(bool(flooding)))
     return dict(bits=bits, iters=iters, success=succ, L=Lo, E=Eo)
 
 

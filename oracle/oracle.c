@@ -429,8 +429,11 @@ finish:
 typedef struct {
     const orc_code* c; const double* llr; const uint8_t* syn; int T, es;
     uint8_t* bits; int32_t* iters; uint8_t* succ; double* L; double* E;
-    int64_t F; int64_t next; pthread_mutex_t mu;
+    int64_t F; int64_t next; pthread_mutex_t mu; int flooding;
 } batch_job_f;
+
+int orc_decode_float_flooding(const orc_code* c, const double* llr, const uint8_t* syn, int T, int early_stop,
+                              uint8_t* bits, int32_t* iters, uint8_t* success, double* L_out, double* E_out);
 
 static void* batch_worker_f(void* p) {
     batch_job_f* b = (batch_job_f*)p;
@@ -441,16 +444,18 @@ static void* batch_worker_f(void* p) {
         int64_t f = b->next++;
         pthread_mutex_unlock(&b->mu);
         if (f >= b->F) break;
-        orc_decode_float(c, b->llr + f * c->n, b->syn + f * sb, b->T, b->es, b->bits + f * nb, b->iters + f,
-                         b->succ + f, b->L ? b->L + f * c->n_edges : NULL, b->E ? b->E + f * c->n : NULL);
+        (b->flooding ? orc_decode_float_flooding : orc_decode_float)(
+            c, b->llr + f * c->n, b->syn + f * sb, b->T, b->es, b->bits + f * nb, b->iters + f, b->succ + f,
+            b->L ? b->L + f * c->n_edges : NULL, b->E ? b->E + f * c->n : NULL);
     }
     return NULL;
 }
 
 int orc_decode_float_batch(const orc_code* c, int64_t F, const double* llr, const uint8_t* syn, int T,
                            int early_stop, uint8_t* bits, int32_t* iters, uint8_t* success, double* L_out,
-                           double* E_out, int nthreads) {
+                           double* E_out, int nthreads, int flooding) {
     batch_job_f b = { c, llr, syn, T, early_stop, bits, iters, success, L_out, E_out, F, 0 };
+    b.flooding = flooding;
     pthread_mutex_init(&b.mu, NULL);
     if (nthreads < 1) nthreads = 1;
     if (nthreads > 512) nthreads = 512;
@@ -458,5 +463,48 @@ int orc_decode_float_batch(const orc_code* c, int64_t F, const double* llr, cons
     for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, batch_worker_f, &b);
     for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
     pthread_mutex_destroy(&b.mu);
+    return 0;
+}
+
+/* Flooding schedule of the same exact BP ("layered scheduling ... enables the
+ * decoding convergence to speed-up by a factor of two" over "original flooding scheduling").  Every
+ * iteration: all check nodes from the previous iteration's state, x_ij = E_j - L_ij (Eq.(8)), then
+ * E_j = channel LLR_j + sum_i L_ij (Eq.(9) over all of VN_j's checks at once), summed in ascending
+ * check order.  Same stopping rule and outputs as orc_decode_float. */
+int orc_decode_float_flooding(const orc_code* c, const double* llr, const uint8_t* syn, int T, int early_stop,
+                              uint8_t* bits, int32_t* iters, uint8_t* success, double* L_out, double* E_out) {
+    int64_t n = c->n;
+    double* E = (double*)malloc(sizeof(double) * n);
+    double* L = (double*)calloc((size_t)c->n_edges, sizeof(double));
+    double x[256], Ln[256];
+    for (int64_t j = 0; j < n; j++) E[j] = llr[j];
+    int t_done = 0, ok = 0;
+    if (early_stop && syndrome_ok_f(c, E, syn)) { ok = 1; goto finish; }
+    for (int t = 1; t <= T; t++) {
+        for (int I = 0; I < c->Mb; I++)                       /* all check nodes, old E and L */
+            for (int r = 0; r < c->Z; r++) {
+                int d = c->deg[I];
+                int64_t i = (int64_t)I * c->Z + r;
+                int s_i = (syn[i >> 3] >> (i & 7)) & 1;
+                for (int k = 0; k < d; k++) x[k] = E[col_of(c, I, r, k)] - L[edge_of(c, I, r, k)];
+                orc_check_node_float(d, x, s_i, Ln);
+                for (int k = 0; k < d; k++) L[edge_of(c, I, r, k)] = Ln[k];   /* E untouched in this pass */
+            }
+        for (int64_t j = 0; j < n; j++) E[j] = llr[j];         /* all variable nodes */
+        for (int I = 0; I < c->Mb; I++)
+            for (int r = 0; r < c->Z; r++)
+                for (int k = 0; k < c->deg[I]; k++) E[col_of(c, I, r, k)] += L[edge_of(c, I, r, k)];
+        t_done = t;
+        if (early_stop && syndrome_ok_f(c, E, syn)) { ok = 1; goto finish; }
+    }
+    ok = early_stop ? 0 : syndrome_ok_f(c, E, syn);
+finish:
+    memset(bits, 0, (size_t)((n + 7) / 8));
+    for (int64_t j = 0; j < n; j++) if (E[j] < 0.0) bits[j >> 3] |= (uint8_t)(1u << (j & 7));
+    *iters = t_done;
+    *success = (uint8_t)ok;
+    if (L_out) memcpy(L_out, L, sizeof(double) * (size_t)c->n_edges);
+    if (E_out) memcpy(E_out, E, sizeof(double) * (size_t)n);
+    free(E); free(L);
     return 0;
 }

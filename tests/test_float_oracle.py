@@ -92,3 +92,36 @@ def test_float_decoder_invariants():
     assert ok.mean() > 0.9 and np.array_equal(code.syndrome(r["bits"][ok]), syn[ok])
     r0 = oracle.decode_float(code, oracle.build_llr_float(code.n, w.qber, x), syn, w.max_iter, 1)
     assert (r0["iters"] == 0).all() and np.array_equal(r0["bits"], x)
+
+
+@pytest.mark.parametrize("shifts,T", [
+    ([[0, 0, 0, -1, -1], [-1, -1, 0, 0, 0]], 3),
+    ([[0, 0, 0, -1, -1, -1, -1], [-1, -1, 0, 0, 0, -1, -1], [-1, -1, -1, -1, 0, 0, 0]], 5),
+])
+def test_flooding_bp_is_exact_on_trees(shifts, T):
+    """The flooding schedule reaches the same exact posteriors on a tree."""
+    sh = np.array(shifts, dtype=np.int32)
+    code = oracle.Code(sh, 1)
+    H = (sh >= 0).astype(int)
+    rng = np.random.default_rng(99 + T)
+    for trial in range(10):
+        llr = rng.normal(0, 2.5, code.n)
+        s = rng.integers(0, 2, code.m)
+        syn = np.packbits(s.astype(np.uint8), bitorder="little")
+        r = oracle.decode_float(code, llr[None], syn[None], T, 0, flooding=True)
+        assert np.allclose(r["E"][0], _exact_posterior(H, llr, s), rtol=1e-9, atol=1e-9)
+
+
+def test_flooding_equals_layered_with_one_layer():
+    """With one block row no variable is shared between layers, so both schedules coincide."""
+    import synth
+
+    sh = synth.qc_code(1, 6, 32, {1: 1.0}, 5)
+    code = oracle.Code(sh, 32)
+    rng = np.random.default_rng(1)
+    llr = rng.normal(0, 3, (4, code.n))
+    syn = rng.integers(0, 256, (4, (code.m + 7) // 8), dtype=np.uint8)
+    a = oracle.decode_float(code, llr, syn, 5, 0)
+    b = oracle.decode_float(code, llr, syn, 5, 0, flooding=True)
+    for k in ("E", "L"):   # equal up to rounding: layered forms E - L + L_new, flooding llr + L_new
+        assert np.allclose(a[k], b[k], rtol=1e-12, atol=1e-12)
