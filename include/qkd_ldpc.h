@@ -176,12 +176,15 @@ int qkd_reconcile_adaptive(const qkd_code* code, double qber, int64_t n_frames,
  *   shortened positions (known_bits required when the code has them).
  * qkd_decode_float_batch: like qkd_decode_batch with float LLRs; final_L_dev (float [F][n_edges],
  *   canonical order) and final_E_dev (float [F][n]) optional.  Check degrees <= 20.
+ *   schedule 0 = layered (the paper's); 1 = flooding: every iteration all
+ *   check nodes from the previous state, then E_j = LLR_j + sum_i L_ij (float atomics, so the
+ *   summation order -- and the last bits of E -- vary from run to run).
  * Errors: QKD_EINVAL, QKD_EDIM (workspace too small), QKD_EUNSUP (degree > 20), QKD_ECUDA. */
 int qkd_build_llr_float(const qkd_code* code, double qber, int64_t n_frames, const uint8_t* bob_bits_dev,
                         const uint8_t* known_bits_dev, float* llr_dev, void* stream);
 size_t qkd_float_workspace_bytes(const qkd_code* code, int64_t n_frames);
 int qkd_decode_float_batch(const qkd_code* code, int64_t n_frames, const float* llr_dev,
-                           const uint8_t* syndrome_dev, int32_t max_iter, int32_t early_stop,
+                           const uint8_t* syndrome_dev, int32_t max_iter, int32_t early_stop, int32_t schedule,
                            void* workspace_dev, size_t workspace_bytes, uint8_t* bits_dev, int32_t* iters_dev,
                            uint8_t* success_dev, float* final_L_dev, float* final_E_dev, void* stream);
 

@@ -54,8 +54,8 @@ def lib():
         L.qkd_build_llr_float.argtypes = [vp, dbl, i64, vp, vp, vp, vp]
         L.qkd_float_workspace_bytes.argtypes = [vp, i64]
         L.qkd_float_workspace_bytes.restype = ctypes.c_size_t
-        L.qkd_decode_float_batch.argtypes = [vp, i64, vp, vp, i32, i32, vp, ctypes.c_size_t, vp, vp, vp, vp, vp,
-                                             vp]
+        L.qkd_decode_float_batch.argtypes = [vp, i64, vp, vp, i32, i32, i32, vp, ctypes.c_size_t, vp, vp, vp, vp,
+                                             vp, vp]
         L.qkd_adaptive_work_bytes.argtypes = [vp, i64]
         L.qkd_adaptive_work_bytes.restype = ctypes.c_size_t
         L.qkd_reconcile_adaptive.argtypes = [vp, dbl, i64, vp, i64, i64, i64, i32, vp, vp, vp, i32, vp,
@@ -227,7 +227,7 @@ class QCCode:
         return out
 
     def decode_float(self, llr, syn, max_iter: int, early_stop: bool = True, want_state: bool = False,
-                     workspace=None, stream=None):
+                     workspace=None, stream=None, flooding: bool = False):
         """qkd_decode_float_batch: dict(bits, iters, success[, L, E]) as cuda tensors (asynchronous)."""
         torch = _torch()
         F = llr.shape[0]
@@ -245,7 +245,7 @@ class QCCode:
                 _check(-6)
             workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         _check(lib().qkd_decode_float_batch(self._h, F, _ptr(llr), _ptr(syn), int(max_iter), int(bool(early_stop)),
-                                            _ptr(workspace), workspace.numel(), _ptr(bits), _ptr(iters), _ptr(succ),
+                                            int(bool(flooding)), _ptr(workspace), workspace.numel(), _ptr(bits), _ptr(iters), _ptr(succ),
                                             _ptr(Lo), _ptr(Eo), _stream(stream)))
         r = dict(bits=bits, iters=iters, success=succ)
         if want_state:

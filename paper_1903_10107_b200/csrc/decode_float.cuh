@@ -95,4 +95,45 @@ __device__ __forceinline__ void row_update_f(const int2* __restrict__ et, int D,
     }
 }
 
+// Flooding schedule: the check-node half of an iteration -- every row from the
+// previous iteration's E and L (Eq.(8)), L_new stored; E is left untouched (the variable-node half,
+// E_j = LLR_j + sum_i L_ij, runs after a barrier).
+__device__ __forceinline__ void row_check_f(const int2* __restrict__ et, int D, int Z, int r, const float* E,
+                                            float* __restrict__ Lrow, int s_i, bool first) {
+    float mg[kFloatDMax], o[kFloatDMax];
+    int sg = s_i, neg = 0;
+#pragma unroll
+    for (int k = 0; k < kFloatDMax; ++k) {
+        if (k < D) {
+            const float xv = E[col_f(et[k], r, Z)] - (first ? 0.0f : Lrow[k]);
+            mg[k] = fabsf(xv);
+            const int nk = xv < 0.0f;
+            neg |= nk << k;
+            sg ^= nk;
+        }
+    }
+    if (D == 1) {
+        o[0] = kLlrKnown;
+    } else {
+        float F[kFloatDMax];
+        F[0] = mg[0];
+#pragma unroll
+        for (int k = 1; k < kFloatDMax; ++k)
+            if (k < D - 1) F[k] = beta_f(F[k - 1], mg[k]);
+        float b = mg[D - 1];
+        o[D - 1] = F[D - 2];
+#pragma unroll
+        for (int k = kFloatDMax - 2; k >= 1; --k) {
+            if (k <= D - 2) {
+                o[k] = beta_f(F[k - 1], b);
+                b = beta_f(mg[k], b);
+            }
+        }
+        o[0] = b;
+    }
+#pragma unroll
+    for (int k = 0; k < kFloatDMax; ++k)
+        if (k < D) Lrow[k] = ((sg ^ (neg >> k)) & 1) ? -o[k] : o[k];
+}
+
 }  // namespace qkd

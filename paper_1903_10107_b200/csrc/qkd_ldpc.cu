@@ -528,7 +528,7 @@ __global__ void scatter_results_kernel(const int32_t* __restrict__ idx, long lon
 // --------------------------------------------------------------------------------------
 // exact floating-point layered BP (decode_float.cuh): one frame per slot
 // --------------------------------------------------------------------------------------
-template <bool ESM>
+template <bool ESM, bool FLOOD>
 __global__ void __launch_bounds__(1024, 1) decode_float_kernel(const FParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     int4* s_layer = reinterpret_cast<int4*>(smem + p.tab_off);
@@ -579,11 +579,31 @@ __global__ void __launch_bounds__(1024, 1) decode_float_kernel(const FParams p) 
         if (p.early_stop) ok = syndrome_ok();   // iteration-0 check (R10)
         while (!ok && it < p.T) {
             ++it;
-            for (int I = 0; I < p.Mb; ++I) {
-                const int4 li = s_layer[I];
-                for (int r = t; r < p.Z; r += p.TG)
-                    row_update_f(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
-                                 sSyn[I * p.Z + r], it == 1);
+            if constexpr (!FLOOD) {   // layered: each block row sees the previous ones' E
+                for (int I = 0; I < p.Mb; ++I) {
+                    const int4 li = s_layer[I];
+                    for (int r = t; r < p.Z; r += p.TG)
+                        row_update_f(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
+                                     sSyn[I * p.Z + r], it == 1);
+                    group_bar(bar, p.TG);
+                }
+            } else {                  // flooding (N4): all checks from the old state, then all VNs
+                for (int I = 0; I < p.Mb; ++I) {
+                    const int4 li = s_layer[I];
+                    for (int r = t; r < p.Z; r += p.TG)
+                        row_check_f(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
+                                    sSyn[I * p.Z + r], it == 1);
+                }
+                group_bar(bar, p.TG);
+                for (int j = t; j < p.n; j += p.TG) E[j] = p.llr[f * p.n + j];
+                group_bar(bar, p.TG);
+                for (int I = 0; I < p.Mb; ++I) {   // E_j = LLR_j + sum_i L_ij (float atomics: order varies)
+                    const int4 li = s_layer[I];
+                    for (int r = t; r < p.Z; r += p.TG) {
+                        const float* Lrow = Ls + li.z + (long long)r * li.w;
+                        for (int k = 0; k < li.x; ++k) atomicAdd(&E[col_f(s_edge[li.y + k], r, p.Z)], Lrow[k]);
+                    }
+                }
                 group_bar(bar, p.TG);
             }
             if (p.early_stop) ok = syndrome_ok();
@@ -1167,9 +1187,13 @@ static int make_fplan(const qkd_code* c, long long F, FPlan& pl) {
     pl.GPC = gpc;
     pl.tab_off = gpc * pl.slot_bytes;
     pl.smem = pl.tab_off + (int)tab;
-    const void* k = pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true>)
-                           : reinterpret_cast<const void*>(&decode_float_kernel<false>);
-    QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+    for (const void* k : {reinterpret_cast<const void*>(&decode_float_kernel<true, false>),
+                          reinterpret_cast<const void*>(&decode_float_kernel<true, true>),
+                          reinterpret_cast<const void*>(&decode_float_kernel<false, false>),
+                          reinterpret_cast<const void*>(&decode_float_kernel<false, true>)})
+        QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+    const void* k = pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true, false>)
+                           : reinterpret_cast<const void*>(&decode_float_kernel<false, false>);
     int per_sm = 0;
     QKD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.TG * pl.GPC, pl.smem));
     if (per_sm < 1) return fail(QKD_EUNSUP, "float decoder cannot be resident with this geometry");
@@ -1202,9 +1226,9 @@ int qkd_build_llr_float(const qkd_code* c, double qber, int64_t F, const uint8_t
 }
 
 int qkd_decode_float_batch(const qkd_code* c, int64_t F, const float* llr, const uint8_t* syn, int32_t max_iter,
-                           int32_t early_stop, void* ws, size_t ws_bytes, uint8_t* bits, int32_t* iters,
-                           uint8_t* success, float* fL, float* fE, void* stream) {
-    if (!c || F < 0 || max_iter < 0) return fail(QKD_EINVAL, "bad argument");
+                           int32_t early_stop, int32_t schedule, void* ws, size_t ws_bytes, uint8_t* bits,
+                           int32_t* iters, uint8_t* success, float* fL, float* fE, void* stream) {
+    if (!c || F < 0 || max_iter < 0 || schedule < 0 || schedule > 1) return fail(QKD_EINVAL, "bad argument");
     if (F == 0) return QKD_OK;
     if (!llr || !syn || !ws || !bits || !iters || !success) return fail(QKD_EINVAL, "null buffer");
     FPlan pl;
@@ -1246,8 +1270,10 @@ int qkd_decode_float_batch(const qkd_code* c, int64_t F, const float* llr, const
     cudaStream_t st = (cudaStream_t)stream;
     QKD_CK(cudaMemsetAsync(p.work, 0, sizeof(int), st));
     void* args[] = {&p};
-    const void* k = pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true>)
-                           : reinterpret_cast<const void*>(&decode_float_kernel<false>);
+    const void* k = schedule ? (pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true, true>)
+                                       : reinterpret_cast<const void*>(&decode_float_kernel<false, true>))
+                             : (pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true, false>)
+                                       : reinterpret_cast<const void*>(&decode_float_kernel<false, false>));
     QKD_CK(cudaLaunchKernel(k, dim3(pl.grid), dim3(pl.TG * pl.GPC), args, pl.smem, st));
     QKD_CK(cudaGetLastError());
     return QKD_OK;

@@ -67,3 +67,33 @@ def test_float_zero_error_frames(gpu):
     g = code.decode_float(code.build_llr_float(w.qber, torch.from_numpy(x).cuda()), torch.from_numpy(syn).cuda(),
                           w.max_iter, True)
     assert (g["iters"].cpu().numpy() == 0).all() and np.array_equal(g["bits"].cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("name,F", [("C1", 16), ("C2", 6)])
+def test_flooding_few_sweeps(gpu, name, F):
+    """Flooding schedule vs the fp64 oracle's flooding, same tolerance."""
+    import torch
+
+    w, oc, x, y, syn = _inputs(name, F)
+    llr_o = oracle.build_llr_float(oc.n, w.qber, y)
+    code = gpu.QCCode(w.shifts(), w.Z)
+    llr_g = code.build_llr_float(w.qber, torch.from_numpy(y).cuda())
+    for T in (1, 2, 3):
+        o = oracle.decode_float(oc, llr_o, syn, T, 0, flooding=True)
+        g = code.decode_float(llr_g, torch.from_numpy(syn).cuda(), T, False, want_state=True, flooding=True)
+        for k in ("E", "L"):
+            gv = g[k].cpu().numpy()
+            assert np.allclose(gv, o[k], rtol=1e-5, atol=2e-3 * T), (k, T, np.abs(gv - o[k]).max())
+
+
+def test_flooding_full_decodes(gpu):
+    import torch
+
+    w, oc, x, y, syn = _inputs("C1", 64)
+    o = oracle.decode_float(oc, oracle.build_llr_float(oc.n, w.qber, y), syn, w.max_iter, 1, flooding=True)
+    code = gpu.QCCode(w.shifts(), w.Z)
+    g = code.decode_float(code.build_llr_float(w.qber, torch.from_numpy(y).cuda()), torch.from_numpy(syn).cuda(),
+                          w.max_iter, True, flooding=True)
+    g = {k: v.cpu().numpy() for k, v in g.items()}
+    same = (g["iters"] == o["iters"]) & (g["success"] == o["success"]) & (g["bits"] == o["bits"]).all(axis=1)
+    assert same.mean() >= 0.95, same.mean()

@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Quantized (improved RCBP + saturation, the product path) vs exact floating-point BP on the same
+"""Quantized (improved RCBP + saturation, the product path) vs exact floating-point BP (layered, and
+flooding: SURVEY §8(f) N4) on the same
 frames ("maintain the high efficiency as the floating-point version").
 
   python tools/float_vs_quant.py [--frames 4096] [--out gpurun_out/float_vs_quant.json]
@@ -62,13 +63,14 @@ def main():
         xs, ys = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         syn = code.syndrome(xs)
         res = {}
-        for kind in ("quantized", "float"):
+        for kind in ("quantized", "float", "float_flooding"):
             if kind == "quantized":
                 llr = code.build_llr(q, ys)
                 run = lambda: code.decode(llr, syn, w.max_iter, True)          # noqa: E731
             else:
                 llr = code.build_llr_float(q, ys)
-                run = lambda: code.decode_float(llr, syn, w.max_iter, True)    # noqa: E731
+                fl = kind == "float_flooding"
+                run = lambda: code.decode_float(llr, syn, w.max_iter, True, flooding=fl)    # noqa: E731
             run()
             torch.cuda.synchronize()
             r, ms = timed(run)
