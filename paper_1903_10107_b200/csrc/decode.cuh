@@ -28,6 +28,7 @@ struct DecParams {
     const uint8_t* syn;       // [F][mb8]
     long long F, ngroups;
     int T, early_stop, vec_llr;
+    int refill;               // per-frame lane refill (early_stop only, not the lane-pair variant)
     uint32_t* Lws;            // [slots][ws_words]
     uint32_t* Ews;            // [slots][n]   (global-E variant only)
     int* work;                // group work counter
@@ -158,6 +159,8 @@ __device__ __forceinline__ uint32_t& w4(uint4& v, int i) { return i == 0 ? v.x :
 
 // One check row r of a block row with D edges (layered update, Alg. 1/2).
 //   et   : the row's D (cb, s) entries;  Lrow : this row's Dp words;  nib : target syndrome bits
+//   first: all four lanes start a frame with this sweep -- messages are L = 0 (R16), not loaded.
+//   (A lane refilled alone has its bytes of the workspace reset to T = 192 when its frame is loaded.)
 template <int D, bool ESM, bool POW2, int KEEP_ADDR_MAX = 10>
 __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, uint32_t r4, uint32_t zm4,
                                            unsigned char* Eb, uint32_t* __restrict__ Lrow, uint32_t nib,

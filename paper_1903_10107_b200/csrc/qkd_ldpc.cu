@@ -72,8 +72,9 @@ constexpr int kFramesPerGroup = 4;
 
 template <int DMAX, bool ESM, bool POW2, bool SPLIT>
 __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, const int2* et, int t,
-                                           unsigned char* Eb, uint32_t* Lslot, const uint8_t* synI, bool first,
+                                           unsigned char* Eb, uint32_t* Lslot, const uint8_t* synI, uint32_t fresh,
                                            const Konst& K) {
+    const bool first = fresh == 0xFu;   // all four lanes on their first sweep: L = 0 without loading
     const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
     if constexpr (SPLIT) {
         // lane pairs: warp-uniform trip count (the shuffles need all 32 lanes), 16 rows per warp pass
@@ -181,11 +182,13 @@ __device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int4
 
 // write the outputs of the lanes in `mask` (state at their stopping iteration)
 __device__ void finalize(const DecParams& p, const int4* s_layer, const uint32_t* Eslot, const uint32_t* Lslot,
-                         long long f0, uint32_t mask, int it, uint32_t succ_mask, bool first, int t) {
+                         const long long* fr, uint32_t mask, const int* itv, uint32_t succ_mask, uint32_t fresh, int t) {
     const int lane = threadIdx.x & 31;
     for (int f = 0; f < kFramesPerGroup; ++f) {
         if (!((mask >> f) & 1u)) continue;
-        const long long frame = f0 + f;
+        const long long frame = fr[f];
+        const int it = itv[f];
+        const bool first = (fresh >> f) & 1u;
         uint8_t* brow = p.bits + frame * p.nb8;
         for (int jw = t & ~31; jw < p.n; jw += p.TG) {
             const int j = jw + lane;
@@ -229,7 +232,7 @@ __device__ void finalize(const DecParams& p, const int4* s_layer, const uint32_t
     }
 }
 
-template <int DMAX, bool ESM, bool POW2, bool SPLIT>
+template <int DMAX, bool ESM, bool POW2, bool SPLIT, bool REFILL>
 __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1)
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -276,13 +279,167 @@ __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 
     uint32_t* flags = reinterpret_cast<uint32_t*>(ctl + 1);
     uint32_t* Lslot = p.Lws + gslot * p.ws_words;
 
-    for (;;) {
+    if constexpr (!SPLIT && REFILL) {
+        // ---- per-frame scheduling: a lane whose frame stops is refilled with the next frame at
+        // once (frames are taken one at a time from p.work), so a slot never waits for the
+        // slowest of its 4 frames.  Lanes never interact, so every frame's result is the same as
+        // in a fresh group.
+        // per-lane frame ids and start sweeps live in shared memory (written by thread 0 before a
+        // barrier): registers stay with the row updates
+        int* s_fr = ctl + 4;        // [4] frame id per lane (-1: none; frames < 2^31, p.work is an int)
+        int* s_start = ctl + 8;     // [4] this slot's sweep count when the lane's frame was loaded
+        uint32_t active = 0, fresh = 0;
+        int chk = 0, sweeps = 0;
+        auto lane_state = [&](long long* fr, int* itv) {
+            for (int f = 0; f < 4; ++f) {
+                fr[f] = s_fr[f];
+                itv[f] = sweeps - s_start[f];
+            }
+        };
+        // take up to popc(mask) new frames into the lanes of `mask`; returns the lanes that got one
+        auto refill_lanes = [&](uint32_t mask) -> uint32_t {
+            const int k = __popc(mask);
+            if (t == 0) ctl[0] = atomicAdd(p.work, k);
+            group_bar(bar, p.TG);
+            const long long a = *(volatile int*)&ctl[0];
+            long long fid[4];
+            uint32_t got = 0;
+            int q = 0;
+            for (int f = 0; f < 4; ++f) {
+                fid[f] = -1;
+                if (!((mask >> f) & 1u)) continue;
+                const long long v = a + q++;
+                if (v < p.F) { fid[f] = v; got |= 1u << f; }
+            }
+            if (t == 0)
+                for (int f = 0; f < 4; ++f)
+                    if ((mask >> f) & 1u) { s_fr[f] = (int)fid[f]; s_start[f] = sweeps; }
+            if (got == 0xFu && p.vec_llr) {
+                // all four lanes, frames a..a+3: 32-bit loads transposed into frame-interleaved
+                // words (E + 127 = (llr ^ 0x80) - 1), and the messages reset by plain stores
+                const long long f0 = fid[0];
+                const int n4 = p.n >> 2;
+                for (int q = t; q < n4; q += p.TG) {
+                    uint32_t r[4];
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) r[f] = __ldcs(reinterpret_cast<const uint32_t*>(p.llr + (f0 + f) * p.n) + q);
+                    const uint32_t pa = prmt<0x5140u>(r[0], r[1]), pb = prmt<0x5140u>(r[2], r[3]);
+                    const uint32_t pc = prmt<0x7362u>(r[0], r[1]), pd = prmt<0x7362u>(r[2], r[3]);
+                    Eslot[4 * q + 0] = (prmt<0x5410u>(pa, pb) ^ 0x80808080u) - 0x01010101u;
+                    Eslot[4 * q + 1] = (prmt<0x7632u>(pa, pb) ^ 0x80808080u) - 0x01010101u;
+                    Eslot[4 * q + 2] = (prmt<0x5410u>(pc, pd) ^ 0x80808080u) - 0x01010101u;
+                    Eslot[4 * q + 3] = (prmt<0x7632u>(pc, pd) ^ 0x80808080u) - 0x01010101u;
+                }
+                // no message reset: the next sweep is every lane's first (fresh == 0xF) and uses L = 0
+            } else if (got) {
+                unsigned char* E8 = reinterpret_cast<unsigned char*>(Eslot);
+#pragma unroll 4
+                for (int j = t; j < p.n; j += p.TG) {          // E byte lane f <- LLR (stored as E + 127)
+#pragma unroll
+                    for (int f = 0; f < 4; ++f)
+                        if ((got >> f) & 1u) E8[4 * j + f] = (uint8_t)(((uint8_t)p.llr[fid[f] * p.n + j] ^ 0x80u) - 1u);
+                }
+                const uint32_t Mg = fresh_mask(got);           // this slot's messages of those lanes: L = 0
+                long long w = t;
+                for (; w + 7LL * p.TG < p.ws_words; w += 8LL * p.TG) {   // 8 independent loads in flight
+                    uint32_t v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = Lslot[w + (long long)u * p.TG];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) Lslot[w + (long long)u * p.TG] = lop3<0xB8>(v[u], Mg, 0xC0C0C0C0u);
+                }
+                for (; w < p.ws_words; w += p.TG) Lslot[w] = lop3<0xB8>(Lslot[w], Mg, 0xC0C0C0C0u);
+            }
+            if (got) {
+                for (int i = t; i < p.m; i += p.TG) {          // syndrome nibble bit f (bits 4-7 kept 0:
+                    uint32_t b = sSyn[i] & 0xFu;               // nib_to_bit6/7 multiply the whole byte)
+#pragma unroll
+                    for (int f = 0; f < 4; ++f)
+                        if ((got >> f) & 1u)
+                            b = (b & ~(1u << f)) | (((uint32_t)(p.syn[fid[f] * p.mb8 + (i >> 3)] >> (i & 7)) & 1u) << f);
+                    sSyn[i] = (uint8_t)b;
+                }
+            }
+            group_bar(bar, p.TG);
+            return got;
+        };
+        auto finish = [&](uint32_t mask, uint32_t succ, uint32_t zeroL) {
+            long long fr[4];
+            int itv[4];
+            lane_state(fr, itv);
+            finalize(p, s_layer, Eslot, Lslot, fr, mask, itv, succ, zeroL, t);
+            group_bar(bar, p.TG);
+        };
+        if (t == 0) { flags[0] = 0; flags[1] = 0; }
+        uint32_t pend = refill_lanes(0xFu);
+        active = fresh = pend;
+        if (!p.early_stop) pend = 0;
+        while (active) {
+            while (pend) {   // iteration-0 check of newly loaded frames (R10)
+                const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, pend);
+                const uint32_t done0 = pend & ~viol;
+                pend = 0;
+                if (done0) {
+                    finish(done0, done0, done0);
+                    active &= ~done0;
+                    const uint32_t got = refill_lanes(done0);
+                    active |= got;
+                    fresh |= got;
+                    pend = got;
+                }
+            }
+            uint32_t cap = 0;   // lanes out of sweeps stop with their state after sweep T (R12)
+            for (int f = 0; f < 4; ++f)
+                if (((active >> f) & 1u) && sweeps - s_start[f] >= p.T) cap |= 1u << f;
+            if (cap) {
+                // early_stop: failure; otherwise success = syndrome matched after sweep T
+                const uint32_t succ = p.early_stop ? 0u
+                    : cap & ~syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, cap);
+                finish(cap, succ, fresh & cap);
+                active &= ~cap;
+                fresh &= ~cap;
+                const uint32_t got = refill_lanes(cap);
+                active |= got;
+                fresh |= got;
+                pend = p.early_stop ? got : 0u;
+                continue;
+            }
+            if (!active) break;
+            for (int I = 0; I < p.Mb; ++I) {   // idle lanes (no frame left) compute harmlessly
+                const int4 li = s_layer[I];
+                layer_pass<DMAX, ESM, POW2, SPLIT>(p, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,
+                                                   fresh == 0xFu ? 0xFu : 0u, K);
+                group_bar(bar, p.TG);
+            }
+            ++sweeps;
+            fresh = 0;
+            if (!p.early_stop) continue;
+            const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
+            const uint32_t done = active & ~viol;
+            if (done) {
+                finish(done, done, 0u);
+                active &= ~done;
+                const uint32_t got = refill_lanes(done);
+                active |= got;
+                fresh |= got;
+                pend = got;
+            }
+        }
+    } else {
+    for (;;) {   // whole 4-frame groups: a slot takes the next 4 frames when all of its lanes stop
         if (t == 0) ctl[0] = atomicAdd(p.work, 1);
         group_bar(bar, p.TG);
         const long long g = *(volatile int*)&ctl[0];
         if (g >= p.ngroups) break;
         const long long f0 = g * kFramesPerGroup;
         const int nl = (int)min((long long)kFramesPerGroup, p.F - f0);
+        // frames f0 + f, all with the group's sweep count (built at each finalize call, not kept live)
+        auto fin = [&](uint32_t mask, int it, uint32_t succ, uint32_t zeroL) {
+            long long fr[4];
+            int itv[4];
+            for (int f = 0; f < 4; ++f) { fr[f] = f0 + f; itv[f] = it; }
+            finalize(p, s_layer, Eslot, Lslot, fr, mask, itv, succ, zeroL, t);
+        };
 
         // ---- E <- channel LLR, frame-interleaved, stored as E + 127 = (llr ^ 0x80) - 1
         if (p.vec_llr) {
@@ -335,7 +492,7 @@ __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 
             const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
             const uint32_t done = active & ~viol;
             if (done) {
-                finalize(p, s_layer, Eslot, Lslot, f0, done, 0, done, true, t);
+                fin(done, 0, done, 0xFu);
                 group_bar(bar, p.TG);
             }
             active &= viol;
@@ -343,18 +500,18 @@ __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 
         int it = 0;
         while (active && it < p.T) {
             ++it;
-            const bool first = it == 1;
+            const uint32_t fresh = it == 1 ? 0xFu : 0u;
             for (int I = 0; I < p.Mb; ++I) {
                 const int4 li = s_layer[I];
                 layer_pass<DMAX, ESM, POW2, SPLIT>(p, li, SPLIT ? s_edge2 + s_soff[I] : s_edge + li.y, t, Eb, Lslot,
-                                                   sSyn + I * p.Z, first, K);
+                                                   sSyn + I * p.Z, fresh, K);
                 group_bar(bar, p.TG);
             }
             if (p.early_stop) {
                 const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
                 const uint32_t done = active & ~viol;
                 if (done) {
-                    finalize(p, s_layer, Eslot, Lslot, f0, done, it, done, false, t);
+                    fin(done, it, done, 0u);
                     group_bar(bar, p.TG);
                 }
                 active &= viol;
@@ -364,9 +521,10 @@ __global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 
             uint32_t succ = 0;
             if (!p.early_stop)
                 succ = active & ~syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
-            finalize(p, s_layer, Eslot, Lslot, f0, active, it, succ, it == 0, t);
+            fin(active, it, succ, it == 0 ? 0xFu : 0u);
         }
         group_bar(bar, p.TG);
+    }
     }
 }
 
@@ -684,12 +842,21 @@ DevInfo dev_info(int dev) {
     return cache[dev];
 }
 
-template <int DMAX, bool ESM, bool POW2, bool SPLIT = false>
+template <int DMAX, bool ESM, bool POW2, bool SPLIT = false, bool REFILL = false>
 const void* kfun() {
-    return reinterpret_cast<const void*>(&decode_kernel<DMAX, ESM, POW2, SPLIT>);
+    return reinterpret_cast<const void*>(&decode_kernel<DMAX, ESM, POW2, SPLIT, REFILL>);
 }
 
-const void* kernel_of(int variant, bool pow2) {
+// refill: per-frame lane scheduling (opt-in, QKD_REFILL=1; not for the lane-pair variant)
+const void* kernel_of(int variant, bool pow2, bool refill = false) {
+    if (refill && variant != 5) {
+        switch (variant) {
+            case 1: return pow2 ? kfun<8, true, true, false, true>() : kfun<8, true, false, false, true>();
+            case 2: return pow2 ? kfun<20, true, true, false, true>() : kfun<20, true, false, false, true>();
+            case 3: return kfun<0, true, false, false, true>();
+            default: return kfun<0, false, false, false, true>();
+        }
+    }
     switch (variant) {
         case 1: return pow2 ? kfun<8, true, true>() : kfun<8, true, false>();
         case 2: return pow2 ? kfun<20, true, true>() : kfun<20, true, false>();
@@ -708,7 +875,7 @@ Konst runtime_konst() {
 // message layout).  1: degree <= 8, smem E; 2: degree <= 20, smem E, one row per thread;
 // 5: degree 9..20, smem E, lane-pair rows; 3: generic smem E; 4: generic global E.
 int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem_optin, bool allow_split) {
-    const long long syn_ctl = ((m + 15) & ~15LL) + 16;
+    const long long syn_ctl = ((m + 15) & ~15LL) + 64;
     const long long tab1 = (long long)Mb * (sizeof(int4) + sizeof(int)) + (long long)nbase * 2 * sizeof(int2) +
                            (long long)Mb * sizeof(int2);
     const bool fits = 4LL * n + syn_ctl + tab1 <= smem_optin;
@@ -723,7 +890,7 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     DevInfo di = dev_info(dev);
     if (!di.ok) return fail(QKD_ECUDA, "cannot query device attributes");
     pl.ngroups = (F + kFramesPerGroup - 1) / kFramesPerGroup;
-    const long long syn_ctl = ((c->m + 15) & ~15LL) + 16;
+    const long long syn_ctl = ((c->m + 15) & ~15LL) + 64;   // syndrome nibbles + control words
     const long long e_bytes = 4LL * c->n;
     pl.variant = choose_variant(c->Mb, c->n, c->m, c->nbase, c->maxdeg, di.smem_optin, c->split);
     if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
@@ -753,6 +920,8 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     pl.smem = pl.tab_off + (int)(fixed_tab + gpc * per_slot_tab);
     const void* k = kernel_of(pl.variant, pl.pow2);
     QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+    QKD_CK(cudaFuncSetAttribute(kernel_of(pl.variant, pl.pow2, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                pl.smem));
     int per_sm = 0;
     QKD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.TG * pl.GPC, pl.smem));
     if (per_sm < 1) return fail(QKD_EUNSUP, "decode kernel cannot be resident with this geometry");
@@ -994,6 +1163,10 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
     p.T = max_iter;
     p.early_stop = early_stop ? 1 : 0;
     p.vec_llr = (c->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(llr) & 3) == 0);
+    {   // per-frame lane refill: opt-in (QKD_REFILL=1): -12% time on C5b, +3-9% on C5a (r1v7 notes)
+        const char* env = std::getenv("QKD_REFILL");
+        p.refill = (pl.variant != 5 && env && env[0] == '1') ? 1 : 0;
+    }
     p.work = reinterpret_cast<int*>(w);
     p.Lws = reinterpret_cast<uint32_t*>(w + 256);
     p.Ews = pl.ws_E ? reinterpret_cast<uint32_t*>(w + 256 + pl.ws_L) : nullptr;
@@ -1013,7 +1186,7 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
     QKD_CK(cudaMemsetAsync(p.work, 0, sizeof(int), st));
     const dim3 grid(pl.grid), block(pl.TG * pl.GPC);
     void* args[] = {&p};
-    QKD_CK(cudaLaunchKernel(kernel_of(pl.variant, pl.pow2), grid, block, args, pl.smem, st));
+    QKD_CK(cudaLaunchKernel(kernel_of(pl.variant, pl.pow2, p.refill != 0), grid, block, args, pl.smem, st));
     QKD_CK(cudaGetLastError());
     return QKD_OK;
 }

@@ -117,6 +117,9 @@ __device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi) { return pr
 // byte mask 0xFF where bit 7 of the byte is set
 __device__ __forceinline__ uint32_t bmask7(uint32_t w) { return prmt<0xBA98u>(w, 0u); }
 
+// lane nibble (bit f = frame lane f) -> byte mask 0xFF in byte f
+__device__ __forceinline__ uint32_t fresh_mask(uint32_t nib) { return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu; }
+
 // syndrome nibble (bit f = frame f) -> flag at bit 6 / bit 7 of byte f
 __device__ __forceinline__ uint32_t nib_to_bit6(uint32_t nib) { return (nib * 0x08102040u) & 0x40404040u; }
 __device__ __forceinline__ uint32_t nib_to_bit7(uint32_t nib) { return (nib * 0x10204080u) & 0x80808080u; }

@@ -205,3 +205,32 @@ def test_split_variant_parity_workloads(gpu, monkeypatch, name, F):
     g, code = gpu_decode(gpu, shifts, w.Z, kind, llr, syn, w.max_iter, w.early_stop)
     assert code.launch_info(F)["variant"] == 15
     assert_same(g, oracle_decode(shifts, w.Z, llr, syn, w.max_iter, w.early_stop))
+
+
+@pytest.mark.parametrize("name,F", [("C1", 64), ("C2", 192), ("C3", 12), ("C4@0.08", 4)])
+def test_refill_variant_parity(gpu, monkeypatch, name, F):
+    """Per-frame lane refill (QKD_REFILL=1): every frame's bits, iterations, success and final L/E
+    are the oracle's, whatever frames share its 4-lane group and whenever its lane was refilled."""
+    monkeypatch.setenv("QKD_REFILL", "1")
+    w, shifts, kind, x, y, llr, syn = workload_inputs(name, F)
+    for T, es in ((w.max_iter, 1), (3, 0), (0, 1)):
+        g, code = gpu_decode(gpu, shifts, w.Z, kind, llr, syn, T, es)
+        assert_same(g, oracle_decode(shifts, w.Z, llr, syn, T, es))
+
+
+@pytest.mark.parametrize("case", sorted(TINY))
+def test_refill_variant_edge_cases(gpu, monkeypatch, case):
+    monkeypatch.setenv("QKD_REFILL", "1")
+    shifts, Z = TINY[case]
+    shifts = np.asarray(shifts, dtype=np.int32)
+    Mb, Nb = shifts.shape
+    n, m = Nb * Z, Mb * Z
+    rng = np.random.default_rng(zlib.crc32(f"refill/{case}".encode()))
+    F = 23
+    llr = rng.integers(-127, 128, size=(F, n)).astype(np.int8)
+    llr[::3] = np.where(rng.random((len(llr[::3]), n)) < 0.9, 100, -100)   # some frames converge fast
+    syn = rng.integers(0, 256, size=(F, (m + 7) // 8), dtype=np.uint8)
+    syn[::3] = 0
+    for T, es in ((9, 1), (1, 0)):
+        g, _ = gpu_decode(gpu, shifts, Z, None, llr, syn, T, es)
+        assert_same(g, oracle_decode(shifts, Z, llr, syn, T, es))
