@@ -214,3 +214,87 @@ def workload(name: str) -> Workload:
 
 
 ALL_PARITY_WORKLOADS = ["C1", "C2", "C3"] + [f"C4@{q:g}" for q in C4_QBERS] + ["C5a", "C5b"]
+
+
+# ---------------------------------------------------------------------------
+# Code construction: PEG base masks and girth >= 6 circulant shifts.
+# P:155 "the girth of a LDPC code is at least 6 ... masking matrices are constructed by using
+# standard PEG algorithm"; SPEC code-model peg_mask / girth_of / seeded shift retry.
+# These build alternative codes; BASELINE's configs keep the Q17 rule (qc_code).
+# ---------------------------------------------------------------------------
+def peg_mask(Mb: int, col_degrees, seed: int = 0) -> np.ndarray:
+    """Progressive edge growth on the base graph (Hu, Eleftheriou, Arnold): columns in non-decreasing
+    degree order; each new edge of a column goes to a check outside its current BFS neighbourhood if
+    one exists, else to a check at the largest BFS depth; ties by lowest check degree, then by a
+    seeded order.  Returns a bool mask [Mb][Nb] (column J gets col_degrees[J] distinct checks)."""
+    Nb = len(col_degrees)
+    rng = np.random.default_rng(seed)
+    tie = rng.permutation(Mb)                       # seeded tie order among equal-degree checks
+    mask = np.zeros((Mb, Nb), dtype=bool)
+    cdeg = np.zeros(Mb, dtype=np.int64)
+    for J in sorted(range(Nb), key=lambda j: (col_degrees[j], j)):
+        for e in range(int(col_degrees[J])):
+            if e == 0:
+                cand = np.arange(Mb)
+            else:
+                # BFS from variable J over the current Tanner graph (checks <-> variables)
+                depth = np.full(Mb, -1)
+                frontier_c = list(np.flatnonzero(mask[:, J]))
+                for c in frontier_c:
+                    depth[c] = 0
+                seen_v = {J}
+                d = 0
+                while frontier_c:
+                    nxt_v = {v for c in frontier_c for v in np.flatnonzero(mask[c]) if v not in seen_v}
+                    seen_v |= nxt_v
+                    d += 1
+                    nxt_c = [c for v in nxt_v for c in np.flatnonzero(mask[:, v]) if depth[c] < 0]
+                    nxt_c = sorted(set(nxt_c))
+                    for c in nxt_c:
+                        depth[c] = d
+                    frontier_c = nxt_c
+                free = np.flatnonzero((depth < 0) & ~mask[:, J])
+                cand = free if len(free) else np.flatnonzero((depth == depth.max()) & ~mask[:, J])
+            best = min(cand, key=lambda c: (cdeg[c], tie[c]))
+            mask[best, J] = True
+            cdeg[best] += 1
+    return mask
+
+
+def _creates_4cycle(sh: np.ndarray, Z: int, I: int, J: int, s: int) -> bool:
+    """Would shift s at (I, J) close a 4-cycle with already assigned entries?  A cycle through rows
+    I, I2 and columns J, J2 exists iff s(I,J) - s(I,J2) + s(I2,J2) - s(I2,J) = 0 mod Z."""
+    Mb, Nb = sh.shape
+    for J2 in range(Nb):
+        if J2 == J or sh[I, J2] < 0:
+            continue
+        for I2 in range(Mb):
+            if I2 == I or sh[I2, J] < 0 or sh[I2, J2] < 0:
+                continue
+            if (s - sh[I, J2] + sh[I2, J2] - sh[I2, J]) % Z == 0:
+                return True
+    return False
+
+
+def girth6_shifts(mask: np.ndarray, Z: int, seed: int = 0, tries: int = 1000) -> np.ndarray:
+    """Seeded uniform shifts in row-major order over the mask, each redrawn until it closes no 4-cycle
+    with the entries already placed ("rejected and retried if girth < 6").  Raises if an
+    entry cannot be placed in `tries` draws (Z too small for the mask)."""
+    rng = np.random.default_rng(seed)
+    sh = np.full(mask.shape, -1, dtype=np.int32)
+    for I, J in zip(*np.nonzero(mask)):
+        for _ in range(tries):
+            s = int(rng.integers(0, Z))
+            if not _creates_4cycle(sh, Z, I, J, s):
+                sh[I, J] = s
+                break
+        else:
+            raise ValueError(f"no 4-cycle-free shift for block ({I},{J}) with Z={Z}")
+    return sh
+
+
+def peg_qc_code(Mb: int, Nb: int, Z: int, fracs: dict[int, float], seed: int) -> np.ndarray:
+    """Q17 degree counts (degree_counts), PEG mask, girth >= 6 shifts."""
+    cnt = degree_counts(Nb, fracs)
+    cols = [d for d in sorted(cnt, reverse=True) for _ in range(cnt[d])]
+    return girth6_shifts(peg_mask(Mb, cols, seed), Z, seed + 1)
