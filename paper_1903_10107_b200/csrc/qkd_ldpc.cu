@@ -1163,9 +1163,11 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
     p.T = max_iter;
     p.early_stop = early_stop ? 1 : 0;
     p.vec_llr = (c->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(llr) & 3) == 0);
-    {   // per-frame lane refill: opt-in (QKD_REFILL=1): -12% time on C5b, +3-9% on C5a (r1v7 notes)
+    {   // per-frame lane refill: default for variant 1 (degree <= 8; C5b -11%), opt-in elsewhere
+        // (QKD_REFILL=1; C5a +9%); QKD_REFILL=0 turns it off everywhere
         const char* env = std::getenv("QKD_REFILL");
-        p.refill = (pl.variant != 5 && env && env[0] == '1') ? 1 : 0;
+        const bool on = env ? env[0] == '1' : pl.variant == 1;
+        p.refill = (pl.variant != 5 && on) ? 1 : 0;
     }
     p.work = reinterpret_cast<int*>(w);
     p.Lws = reinterpret_cast<uint32_t*>(w + 256);
