@@ -328,10 +328,12 @@ def run_gpu(args):
                              "alg_GBps": bytes_rank / (t / 1000) / 1e9, "launch": s["info"]}
     dom = max(per_wl, key=lambda k: per_wl[k]["decode_ms"])
     achieved = per_wl[dom]["alg_GBps"]
-    traffic = None
-    try:
+    traffic, ncu = None, None
+    try:   # from the committed ncu capture of this launch (profiles/<tag>_decode_full.md)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get("decode_dram_bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("decode_dram_bytes_per_launch")
+        ncu = dict(tj.get("ncu") or {}, source=tj.get("source"))
     except Exception:
         pass
 
@@ -355,7 +357,7 @@ def run_gpu(args):
                 "config": dict(workload_config(args.workload), parallelism=f"frames sharded over {world} rank(s)",
                                processed_key_mbps=processed, per_workload=per_wl),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": traffic,
+                             "frac": achieved / peak, "traffic": traffic, "ncu": ncu,
                              "kernel": f"decode_kernel ({dom} launch: {per_wl[dom]['decode_ms']:.1f} ms of "
                                        f"{1000 * sec_per_step:.1f} ms per step)",
                              "algorithmic_bytes_per_launch": per_wl[dom]["alg_bytes"],

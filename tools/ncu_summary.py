@@ -126,9 +126,24 @@ def main():
             lines.append("\n" + a.note)
         with open(os.path.join(prof, f"{a.tag}_decode_full.md"), "w") as f:
             f.write("\n".join(lines) + "\n")
+        def num(key):
+            try:
+                return float(first[key])
+            except (KeyError, ValueError):
+                return None
+
+        dur_ms = num("gpu__time_duration.sum")
+        counters = {   # DRAM GB/s, integer-issue fraction and the ALU/FMA pipe split
+            "dram_GBps": dram / (dur_ms * 1e-3) / 1e9 if dur_ms else None,
+            "issue_active_frac": (num("smsp__issue_active.avg.pct_of_peak_sustained_active") or 0) / 100,
+            "alu_pipe_frac": (num("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active") or 0) / 100,
+            "fma_pipe_frac": (num("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active") or 0) / 100,
+            "warp_instructions": num("smsp__inst_executed.sum"),
+            "duration_ms_under_ncu": dur_ms,
+        }
         with open(os.path.join(prof, "traffic.json"), "w") as f:
-            json.dump({"decode_dram_bytes_per_launch": dram, "source": f"profiles/{a.tag}_decode_full.md",
-                       "kernel": first["kernel"]}, f, indent=1)
+            json.dump({"decode_dram_bytes_per_launch": dram, "ncu": counters,
+                       "source": f"profiles/{a.tag}_decode_full.md", "kernel": first["kernel"]}, f, indent=1)
         print("\n".join(lines))
 
 
