@@ -130,7 +130,9 @@ int qkd_score_batch(const qkd_code* code, int64_t n_frames, const uint8_t* bits_
 
 /* End-to-end call with HOST buffers: copies Bob's bits, the known (shortened) bits and
  * Alice's syndrome host->device, builds the LLRs, decodes and copies bits/iters/success back
- * (device->host), all on `stream`; returns after the stream has completed.
+ * (device->host); returns when everything has completed.  The batch is pipelined in chunks: the
+ * copies run on two internal streams chained by events to `stream`, which builds and decodes, so
+ * transfers overlap decoding (host buffers should be pinned for that).
  * device_buffer must hold qkd_reconcile_device_bytes(code, F) bytes. */
 size_t qkd_reconcile_device_bytes(const qkd_code* code, int64_t n_frames);
 int qkd_reconcile_host(const qkd_code* code, double qber, int64_t n_frames,

@@ -1242,18 +1242,57 @@ int qkd_reconcile_host(const qkd_code* c, double qber, int64_t F, const uint8_t*
     uint8_t* d_su = (uint8_t*)w; w += align256(F);
     const size_t wsb = qkd_workspace_bytes(c, F);
     cudaStream_t st = (cudaStream_t)stream;
-    QKD_CK(cudaMemcpyAsync(d_y, y_h, F * nb8, cudaMemcpyHostToDevice, st));
-    if (d_k) QKD_CK(cudaMemcpyAsync(d_k, known_h, F * nb8, cudaMemcpyHostToDevice, st));
-    QKD_CK(cudaMemcpyAsync(d_s, syn_h, F * mb8, cudaMemcpyHostToDevice, st));
-    int rc = qkd_build_llr(c, qber, F, d_y, d_k, d_llr, stream);
+    // Pipelined in K chunks of frames: copies in on one stream, LLR + decode on the caller's stream,
+    // copies out on a third, chained by events, so chunk c's decode overlaps chunk c+1's host->device
+    // and chunk c-1's device->host transfers.  Chunks keep >= ~16 waves of frame groups each (tail
+    // effect per launch), at most 8 of them.
+    Plan pl;
+    int rc = make_plan(c, F, pl);
     if (rc) return rc;
-    rc = qkd_decode_batch(c, F, d_llr, d_s, max_iter, early_stop, w, wsb, d_b, d_it, d_su, nullptr, nullptr, nullptr,
-                          stream);
-    if (rc) return rc;
-    QKD_CK(cudaMemcpyAsync(bits_h, d_b, F * nb8, cudaMemcpyDeviceToHost, st));
-    QKD_CK(cudaMemcpyAsync(iters_h, d_it, F * 4, cudaMemcpyDeviceToHost, st));
-    QKD_CK(cudaMemcpyAsync(succ_h, d_su, F, cudaMemcpyDeviceToHost, st));
-    QKD_CK(cudaStreamSynchronize(st));
+    const long long per_wave = std::max<long long>(1, pl.slots) * kFramesPerGroup;
+    const int K = (int)std::max<long long>(1, std::min<long long>(8, F / (16 * per_wave)));
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev(2 * (size_t)K, nullptr);
+    auto cleanup = [&]() {
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+        if (s_in) cudaStreamDestroy(s_in);
+        if (s_out) cudaStreamDestroy(s_out);
+    };
+    auto ck = [&](cudaError_t e, const char* what) -> int {
+        if (e == cudaSuccess) return QKD_OK;
+        cleanup();
+        return fail(QKD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    if ((rc = ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream"))) return rc;
+    if ((rc = ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream"))) return rc;
+    for (auto& e : ev)
+        if ((rc = ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"))) return rc;
+    for (int k = 0; k < K; ++k) {   // all host->device copies, in chunk order
+        const long long a = F * k / K, n_k = F * (k + 1) / K - a;
+        if ((rc = ck(cudaMemcpyAsync(d_y + a * nb8, y_h + a * nb8, n_k * nb8, cudaMemcpyHostToDevice, s_in), "h2d"))) return rc;
+        if (d_k && (rc = ck(cudaMemcpyAsync(d_k + a * nb8, known_h + a * nb8, n_k * nb8, cudaMemcpyHostToDevice, s_in), "h2d")))
+            return rc;
+        if ((rc = ck(cudaMemcpyAsync(d_s + a * mb8, syn_h + a * mb8, n_k * mb8, cudaMemcpyHostToDevice, s_in), "h2d"))) return rc;
+        if ((rc = ck(cudaEventRecord(ev[2 * k], s_in), "event"))) return rc;
+    }
+    for (int k = 0; k < K; ++k) {
+        const long long a = F * k / K, n_k = F * (k + 1) / K - a;
+        if ((rc = ck(cudaStreamWaitEvent(st, ev[2 * k], 0), "wait"))) return rc;
+        rc = qkd_build_llr(c, qber, n_k, d_y + a * nb8, d_k ? d_k + a * nb8 : nullptr, d_llr + a * (long long)c->n, stream);
+        if (!rc)
+            rc = qkd_decode_batch(c, n_k, d_llr + a * (long long)c->n, d_s + a * mb8, max_iter, early_stop, w, wsb,
+                                  d_b + a * nb8, d_it + a, d_su + a, nullptr, nullptr, nullptr, stream);
+        if (rc) { cleanup(); return rc; }
+        if ((rc = ck(cudaEventRecord(ev[2 * k + 1], st), "event"))) return rc;
+        if ((rc = ck(cudaStreamWaitEvent(s_out, ev[2 * k + 1], 0), "wait"))) return rc;
+        if ((rc = ck(cudaMemcpyAsync(bits_h + a * nb8, d_b + a * nb8, n_k * nb8, cudaMemcpyDeviceToHost, s_out), "d2h")))
+            return rc;
+        if ((rc = ck(cudaMemcpyAsync(iters_h + a, d_it + a, n_k * 4, cudaMemcpyDeviceToHost, s_out), "d2h"))) return rc;
+        if ((rc = ck(cudaMemcpyAsync(succ_h + a, d_su + a, n_k, cudaMemcpyDeviceToHost, s_out), "d2h"))) return rc;
+    }
+    if ((rc = ck(cudaStreamSynchronize(s_out), "sync"))) return rc;
+    if ((rc = ck(cudaStreamSynchronize(st), "sync"))) return rc;
+    cleanup();
     return QKD_OK;
 }
 
