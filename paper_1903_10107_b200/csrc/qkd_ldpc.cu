@@ -561,6 +561,39 @@ __global__ void syndrome_kernel(const int4* __restrict__ layer, const int2* __re
     }
 }
 
+// Z % 32 == 0: syndrome block I = XOR over its blocks J of x_J rotated by s_IJ (bit r of the
+// rotated Z-bit segment is x_J[(r + s) mod Z]), 32 checks per word: word w of the rotation by
+// s = 32 q + t is the funnel shift of words w+q and w+q+1 (mod Z/32) right by t.  One CTA per frame,
+// the frame's words staged in shared memory.
+__global__ void syndrome_qc_kernel(const int4* __restrict__ layer, const int2* __restrict__ edge, int Mb, int Z,
+                                   int nw, int mb8, long long F, const uint8_t* __restrict__ bits,
+                                   uint8_t* __restrict__ syn) {
+    extern __shared__ __align__(16) uint32_t sx[];
+    const int W = Z >> 5;
+    for (long long f = blockIdx.x; f < F; f += gridDim.x) {
+        __syncthreads();
+        const uint32_t* xf = reinterpret_cast<const uint32_t*>(bits + f * (long long)nw * 4);
+        for (int i = threadIdx.x; i < nw; i += blockDim.x) sx[i] = xf[i];
+        __syncthreads();
+        uint32_t* so = reinterpret_cast<uint32_t*>(syn + f * (long long)mb8);
+        for (int idx = threadIdx.x; idx < Mb * W; idx += blockDim.x) {
+            const int I = idx / W, w = idx - I * W;
+            const int4 li = layer[I];
+            uint32_t acc = 0;
+            for (int k = 0; k < li.x; ++k) {
+                const int2 e = edge[li.y + k];            // (J*Z, shift)
+                const int q = e.y >> 5, t = e.y & 31;
+                int w0 = w + q;
+                w0 = w0 >= W ? w0 - W : w0;
+                const int w1 = w0 + 1 == W ? 0 : w0 + 1;
+                const uint32_t* seg = sx + (e.x >> 5);
+                acc ^= __funnelshift_r(seg[w0], seg[w1], t);
+            }
+            so[idx] = acc;
+        }
+    }
+}
+
 // --------------------------------------------------------------------------------------
 // Bob's channel LLRs (P:103-112 quantization, P:157 puncture/shorten)
 // --------------------------------------------------------------------------------------
@@ -568,6 +601,39 @@ __global__ void build_llr_kernel(int n, int nb8, long long F, int Lq, const uint
                                  const uint8_t* __restrict__ known, const uint8_t* __restrict__ kind,
                                  int8_t* __restrict__ llr) {
     const long long total = F * nb8;
+    if ((n & 7) == 0 && (reinterpret_cast<uintptr_t>(llr) & 7) == 0) {
+        // one input byte -> one 8-byte store: bit s of y selects -Lq / +Lq for position 8b + s
+        const uint32_t pos = (uint32_t)(Lq & 0xFF) * 0x01010101u, neg = (uint32_t)(-Lq & 0xFF) * 0x01010101u;
+        for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+             q += (long long)gridDim.x * blockDim.x) {
+            const long long f = q / nb8;
+            const int b = (int)(q - f * nb8);
+            const uint32_t yb = y[q];
+            // byte mask of set bits: bit s -> byte s (0xFF)
+            const uint32_t lo = ((yb & 0x0Fu) * 0x00204081u & 0x01010101u) * 0xFFu;
+            const uint32_t hi = (((yb >> 4) & 0x0Fu) * 0x00204081u & 0x01010101u) * 0xFFu;
+            uint2 v = make_uint2((neg & lo) | (pos & ~lo), (neg & hi) | (pos & ~hi));
+            if (kind) {
+                const uint2 kd = *reinterpret_cast<const uint2*>(kind + 8LL * b);
+                const uint32_t kb = known ? known[q] : 0u;
+                const uint32_t klo = ((kb & 0x0Fu) * 0x00204081u & 0x01010101u) * 0xFFu;
+                const uint32_t khi = (((kb >> 4) & 0x0Fu) * 0x00204081u & 0x01010101u) * 0xFFu;
+                uint32_t w[2] = {v.x, v.y};
+                const uint32_t kw[2] = {kd.x, kd.y}, km[2] = {klo, khi};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    // punctured (1) -> 0, shortened (2) -> +-127 by the known bit (R19)
+                    const uint32_t p1 = ((kw[h] & 0x01010101u) & ~(kw[h] >> 1)) * 0xFFu;   // kind == 1
+                    const uint32_t s2 = ((kw[h] >> 1) & 0x01010101u) * 0xFFu;             // kind == 2
+                    const uint32_t sv = (0x81818181u & km[h]) | (0x7F7F7F7Fu & ~km[h]);
+                    w[h] = (w[h] & ~(p1 | s2)) | (sv & s2);
+                }
+                v = make_uint2(w[0], w[1]);
+            }
+            *reinterpret_cast<uint2*>(llr + f * n + 8LL * b) = v;
+        }
+        return;
+    }
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
          q += (long long)gridDim.x * blockDim.x) {
         const long long f = q / nb8;
@@ -1085,9 +1151,17 @@ int qkd_syndrome(const qkd_code* c, int64_t F, const uint8_t* bits, uint8_t* syn
     const DevInfo di = dev_info(dev);
     QKD_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(&syndrome_kernel),
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, nb8));
+    QKD_CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(&syndrome_qc_kernel),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, nb8));
     const int grid = (int)std::min<long long>(F, (long long)di.sms * 8);
-    syndrome_kernel<<<grid, 256, nb8, (cudaStream_t)stream>>>(c->d_layer, c->d_edge, c->Mb, c->Z, (int)c->n,
-                                                               (int)c->m, nb8, mb8, F, bits, syn);
+    if (c->Z % 32 == 0 && ((reinterpret_cast<uintptr_t>(bits) | reinterpret_cast<uintptr_t>(syn)) & 3) == 0) {
+        // n, m are multiples of 32 here, so frames are whole words
+        syndrome_qc_kernel<<<grid, 256, nb8, (cudaStream_t)stream>>>(c->d_layer, c->d_edge, c->Mb, c->Z, nb8 / 4,
+                                                                     mb8, F, bits, syn);
+    } else {
+        syndrome_kernel<<<grid, 256, nb8, (cudaStream_t)stream>>>(c->d_layer, c->d_edge, c->Mb, c->Z, (int)c->n,
+                                                                   (int)c->m, nb8, mb8, F, bits, syn);
+    }
     QKD_CK(cudaGetLastError());
     return QKD_OK;
 }
