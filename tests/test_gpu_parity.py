@@ -179,6 +179,30 @@ def test_full_size_sampled(gpu, name):
     assert np.array_equal(s_bits[ok], syn.cpu().numpy()[sl][ok])
 
 
+def test_full_size_c5b_every_shard_full_state(gpu):
+    """SURVEY §8(c) parity contract for C5: >= 4096 frames covering every rank's shard (8 ranks x
+    8192 frames), from the full 65536-frame launch in the bench's configuration, bit-exact in bits,
+    iters, success and the final L and E against the oracle."""
+    import torch
+
+    w = synth.workload("C5b")
+    F = w.frames
+    shifts = w.shifts()
+    x, y, _ = w.gen(0, F)
+    code = gpu.QCCode(shifts, w.Z)
+    syn = code.syndrome(torch.from_numpy(x).cuda())
+    llr = code.build_llr(w.qber, torch.from_numpy(y).cuda())
+    r = code.decode(llr, syn, w.max_iter, True, want_state=True)
+    shard = F // 8
+    sample = np.concatenate([np.arange(k * shard, k * shard + 512) for k in range(8)])
+    idx = torch.from_numpy(sample).cuda()
+    g = {k: v.index_select(0, idx).cpu().numpy() for k, v in r.items()}
+    del r
+    oc = oracle.Code(shifts, w.Z)
+    o = oc.decode(oc.build_llr(w.qber, y[sample]), oc.syndrome(x[sample]), w.max_iter, 1)
+    assert_same(g, o)
+
+
 @pytest.mark.parametrize("case", ["deg9to20", "Z96_multiwarp"])
 @pytest.mark.parametrize("F", [1, 7])
 def test_split_variant_parity_edge_cases(gpu, monkeypatch, case, F):
