@@ -334,6 +334,14 @@ def run_gpu(args):
             tj = json.load(f)
         traffic = tj.get("decode_dram_bytes_per_launch")
         ncu = dict(tj.get("ncu") or {}, source=tj.get("source"))
+        if world > 1:   # the capture is of the 1-GPU launch (all frames of the workload)
+            traffic = None
+        elif ncu.get("warp_instructions") and clocks and clocks.get("sm_mhz"):
+            # SURVEY §8(d) co-bound: integer-issue fraction inst_executed / (SMs * 4 * clk * t), with the
+            # captured launch's instruction count (deterministic for this workload) and the live time/clock
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            ncu["int_issue_frac_live"] = ncu["warp_instructions"] / (
+                sms * 4 * clocks["sm_mhz"] * 1e6 * per_wl[dom]["decode_ms"] / 1000)
     except Exception:
         pass
 
