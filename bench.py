@@ -57,6 +57,17 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def shard(F: int, rank: int, world: int) -> tuple[int, int]:
     """Global frame ids [a, b) decoded by `rank` (contiguous, even split)."""
     return rank * F // world, (rank + 1) * F // world
@@ -358,7 +369,13 @@ def run_gpu(args):
             v, _ = extrapolate(names, sm, {n: synth.workload(n).frames for n in names})
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": ", ".join(f"first {per[n]} frames of {n}" for n in names)
-                   + f" ({time.perf_counter() - t0:.1f}s of CPU work), extrapolated to the full workload"}
+                   + f" ({time.perf_counter() - t0:.1f}s of CPU work), extrapolated to the full workload",
+                   "cpu_model": cpu_model()}
+            # single-thread figure beside the all-core one (small sample, ~2-4 s)
+            per1 = {n: max(1, per[n] // max(1, cores) // 4) for n in names}
+            sm1 = oracle_sample(names, per1, 1)
+            cpu["single_thread_value"], _ = extrapolate(names, sm1, {n: synth.workload(n).frames for n in names})
+            cpu["single_thread_sample"] = ", ".join(f"first {per1[n]} frames of {n}" for n in names)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
