@@ -169,6 +169,10 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
     // High degrees recompute each E address in the emit phase (one smem table load + IMAD + LOP3)
     // instead of holding D addresses in registers through the forward/backward passes.
     constexpr bool KEEP_ADDR = D <= KEEP_ADDR_MAX;
+    // Degrees above 20 (the degree <= 32 kernel) keep only cw and the old message word per edge
+    // between the gather and the emit (edge_out_s recomputes x from them): 2 registers per edge
+    // instead of 3, so rows up to degree 32 stay in registers.
+    constexpr bool LOWREG = D > 20;
     uint4 S[NV];
     uint32_t addr[D];
     EdgeIn in[D];
@@ -211,7 +215,10 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         }
         const uint32_t ew = ldE<ESM>(Eb, a);
         uint32_t eo;
-        w4(S[k >> 2], k & 3) = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
+        if constexpr (LOWREG)
+            w4(S[k >> 2], k & 3) = edge_out_s(o, Q ^ in[k].cw, w4(S[k >> 2], k & 3), ew, K, eo);
+        else
+            w4(S[k >> 2], k & 3) = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
         stE<ESM>(Eb, a, eo);
         if (D <= 2 ? (k == 0) : last_of_group(k)) st4(Lrow + (k & ~3), S[k >> 2]);
     };

@@ -112,7 +112,8 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
             QKD_CASE(1) QKD_CASE(2) QKD_CASE(3) QKD_CASE(4) QKD_CASE(5) QKD_CASE(6) QKD_CASE(7)
             QKD_CASE(8) QKD_CASE(9) QKD_CASE(10) QKD_CASE(11) QKD_CASE(12) QKD_CASE(13)
             QKD_CASE(14) QKD_CASE(15) QKD_CASE(16) QKD_CASE(17) QKD_CASE(18) QKD_CASE(19)
-            QKD_CASE(20)
+            QKD_CASE(20) QKD_CASE(21) QKD_CASE(22) QKD_CASE(23) QKD_CASE(24) QKD_CASE(25) QKD_CASE(26)
+            QKD_CASE(27) QKD_CASE(28) QKD_CASE(29) QKD_CASE(30) QKD_CASE(31) QKD_CASE(32)
 #undef QKD_CASE
             default:
                 break;
@@ -128,6 +129,11 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
 // group-uniform, exact for the lanes in `active`.  Hard decision bit = (E < 0) = NOT bit 7 of
 // (E'' + 1), E'' = E + 127 (R9).  A warp whose own rows already show a violation in every
 // active lane stops early: the group's answer for those lanes ("not yet") cannot change.
+#ifndef QKD_D32_THREADS
+#define QKD_D32_THREADS 512
+#endif
+#define QKD_D32_TG(DMAX) ((DMAX) == 32 ? QKD_D32_THREADS : 512)
+
 template <int DMAX, bool ESM, bool POW2>
 __device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int4* s_layer, const int2* s_edge,
                                                   const unsigned char* Eb, const uint8_t* sSyn, int t,
@@ -233,7 +239,7 @@ __device__ void finalize(const DecParams& p, const int4* s_layer, const uint32_t
 }
 
 template <int DMAX, bool ESM, bool POW2, bool SPLIT, bool REFILL>
-__global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 ? 512 : 256), 1)
+__global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 || DMAX == 32 ? QKD_D32_TG(DMAX) : 256), 1)
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Konst K = p.K.in_regs();
@@ -915,7 +921,7 @@ const void* kfun() {
 
 // refill: per-frame lane scheduling (opt-in, QKD_REFILL=1; not for the lane-pair variant)
 const void* kernel_of(int variant, bool pow2, bool refill = false) {
-    if (refill && variant != 5) {
+    if (refill && variant != 5 && variant != 6) {
         switch (variant) {
             case 1: return pow2 ? kfun<8, true, true, false, true>() : kfun<8, true, false, false, true>();
             case 2: return pow2 ? kfun<20, true, true, false, true>() : kfun<20, true, false, false, true>();
@@ -927,6 +933,7 @@ const void* kernel_of(int variant, bool pow2, bool refill = false) {
         case 1: return pow2 ? kfun<8, true, true>() : kfun<8, true, false>();
         case 2: return pow2 ? kfun<20, true, true>() : kfun<20, true, false>();
         case 3: return kfun<0, true, false>();
+        case 6: return pow2 ? kfun<32, true, true>() : kfun<32, true, false>();
         case 5: return pow2 ? kfun<20, true, true, true>() : kfun<20, true, false, true>();
         default: return kfun<0, false, false>();
     }
@@ -939,7 +946,8 @@ Konst runtime_konst() {
 
 // Decode variant of a code on a device (fixed at code creation: the split variant has its own
 // message layout).  1: degree <= 8, smem E; 2: degree <= 20, smem E, one row per thread;
-// 5: degree 9..20, smem E, lane-pair rows; 3: generic smem E; 4: generic global E.
+// 5: degree 9..20, smem E, lane-pair rows; 6: degree 21..32, smem E, one row per thread;
+// 3: generic smem E; 4: generic global E.
 int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem_optin, bool allow_split) {
     const long long syn_ctl = ((m + 15) & ~15LL) + 64;
     const long long tab1 = (long long)Mb * (sizeof(int4) + sizeof(int)) + (long long)nbase * 2 * sizeof(int2) +
@@ -947,6 +955,7 @@ int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem
     const bool fits = 4LL * n + syn_ctl + tab1 <= smem_optin;
     if (fits && maxdeg <= 8) return 1;
     if (fits && maxdeg <= 20) return allow_split ? 5 : 2;
+    if (fits && maxdeg <= 32 && !std::getenv("QKD_NO_D32")) return 6;
     return fits ? 3 : 4;
 }
 
@@ -960,8 +969,9 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     const long long e_bytes = 4LL * c->n;
     pl.variant = choose_variant(c->Mb, c->n, c->m, c->nbase, c->maxdeg, di.smem_optin, c->split);
     if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
-    pl.pow2 = (pl.variant <= 2 || pl.variant == 5) && ((c->Z & (c->Z - 1)) == 0);
-    const int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024 : (pl.variant == 2 ? 512 : 256);
+    pl.pow2 = (pl.variant <= 2 || pl.variant >= 5) && ((c->Z & (c->Z - 1)) == 0);
+    const int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024
+                       : (pl.variant == 2 ? 512 : (pl.variant == 6 ? QKD_D32_THREADS : 256));
     if (pl.variant == 5)   // two lanes per row, 16 rows per warp
         pl.TG = (int)std::min<long long>(((long long)c->Z + 15) / 16 * 32, tg_max);
     else
@@ -1241,7 +1251,7 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
         // (QKD_REFILL=1; C5a +9%); QKD_REFILL=0 turns it off everywhere
         const char* env = std::getenv("QKD_REFILL");
         const bool on = env ? env[0] == '1' : pl.variant == 1;
-        p.refill = (pl.variant != 5 && on) ? 1 : 0;
+        p.refill = (pl.variant != 5 && pl.variant != 6 && on) ? 1 : 0;
     }
     p.work = reinterpret_cast<int*>(w);
     p.Lws = reinterpret_cast<uint32_t*>(w + 256);

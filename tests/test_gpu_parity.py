@@ -52,12 +52,23 @@ def _tiny_cases():
     sh = rng.integers(0, 40, (3, 30))
     sh[1, rng.random(30) < 0.5] = -1
     sh[2, rng.random(30) < 0.8] = -1
-    cases["deg30_generic"] = (sh, 40)                                              # degree > 20
+    cases["deg30_Z40"] = (sh, 40)                                                  # degree 21..32, Z not pow2
     sh = rng.integers(0, 64, (4, 24))
     sh[rng.random((4, 24)) < 0.4] = -1
     cases["deg9to20"] = (sh, 64)
     sh = rng.integers(0, 96, (3, 9))
     cases["Z96_multiwarp"] = (sh, 96)                                              # Z%32==0, not pow2
+    sh = np.full((4, 36), -1)
+    for I in range(4):                                                             # degrees 21..32 (variant 6)
+        cols = rng.permutation(36)[: int(rng.integers(21, 33))]
+        sh[I, cols] = rng.integers(0, 64, len(cols))
+    sh[0, (sh >= 0).sum(axis=0) == 0] = 5
+    cases["deg21to32_pow2"] = (sh, 64)
+    sh = rng.integers(0, 8, (2, 44))
+    sh[1, rng.random(44) < 0.7] = -1
+    sh[0, :4] = -1
+    sh[1, :4] = rng.integers(0, 8, 4)
+    cases["deg40_generic"] = (sh, 8)                                               # degree > 32
     return cases
 
 
@@ -229,6 +240,45 @@ def test_split_variant_parity_workloads(gpu, monkeypatch, name, F):
     g, code = gpu_decode(gpu, shifts, w.Z, kind, llr, syn, w.max_iter, w.early_stop)
     assert code.launch_info(F)["variant"] == 15
     assert_same(g, oracle_decode(shifts, w.Z, llr, syn, w.max_iter, w.early_stop))
+
+
+@pytest.mark.parametrize("case", ["deg30_Z40", "deg21to32_pow2"])
+def test_degree32_variant_against_generic(gpu, monkeypatch, case):
+    """Degrees 21..32 run on the register kernel (variant 6); QKD_NO_D32=1 forces the generic one:
+    both must equal the oracle."""
+    shifts, Z = TINY[case]
+    shifts = np.asarray(shifts, dtype=np.int32)
+    code = gpu.QCCode(shifts, Z)
+    assert code.launch_info(8)["variant"] % 10 == 6
+    n, m = shifts.shape[1] * Z, shifts.shape[0] * Z
+    rng = np.random.default_rng(zlib.crc32(case.encode()))
+    llr = rng.integers(-127, 128, size=(8, n)).astype(np.int8)
+    syn = rng.integers(0, 256, size=(8, (m + 7) // 8), dtype=np.uint8)
+    o = oracle_decode(shifts, Z, llr, syn, 7, 1)
+    g, _ = gpu_decode(gpu, shifts, Z, None, llr, syn, 7, 1)
+    assert_same(g, o)
+    monkeypatch.setenv("QKD_NO_D32", "1")
+    assert gpu.QCCode(shifts, Z).launch_info(8)["variant"] % 10 == 3
+    g, _ = gpu_decode(gpu, shifts, Z, None, llr, syn, 7, 1)
+    assert_same(g, o)
+
+
+def test_stable_profile_code_parity(gpu):
+    """The best stable degree profile of profiles/r1_degree_profiles.md (check degree 27-28, variant 6)
+    on channel frames at QBER 1.75 %, bit-exact against the oracle."""
+    import torch
+
+    cols = [8] * 16 + [3] * 21 + [2] * 13
+    shifts = synth.girth6_shifts(synth.peg_mask(8, cols, 7), 1024, 8)
+    code = gpu.QCCode(shifts, 1024)
+    assert code.launch_info(8)["variant"] == 16
+    x, y, _ = synth.frames(50 * 1024, 0.0175, 203, 0, 6)
+    oc = oracle.Code(shifts, 1024)
+    syn = oc.syndrome(x)
+    llr = oc.build_llr(0.0175, y)
+    g, _ = gpu_decode(gpu, shifts, 1024, None, llr, syn, 50, 1)
+    o = oracle_decode(shifts, 1024, llr, syn, 50, 1)
+    assert_same(g, o)
 
 
 @pytest.mark.parametrize("name,F", [("C1", 64), ("C2", 192), ("C3", 12), ("C4@0.08", 4)])
