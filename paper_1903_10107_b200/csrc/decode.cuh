@@ -172,7 +172,10 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
     // Degrees above 20 (the degree <= 32 kernel) keep only cw and the old message word per edge
     // between the gather and the emit (edge_out_s recomputes x from them): 2 registers per edge
     // instead of 3, so rows up to degree 32 stay in registers.
-    constexpr bool LOWREG = D > 20;
+#ifndef QKD_LOWREG_MIN
+#define QKD_LOWREG_MIN 21
+#endif
+    constexpr bool LOWREG = D >= QKD_LOWREG_MIN;
     uint4 S[NV];
     uint32_t addr[D];
     EdgeIn in[D];
