@@ -177,7 +177,7 @@ int qkd_reconcile_adaptive(const qkd_code* code, double qber, int64_t n_frames,
  * qkd_build_llr_float: llr_dev float [F][n] = +-ln((1-q)/q) by Bob's bit, 0 punctured, +-1000 for
  *   shortened positions (known_bits required when the code has them).
  * qkd_decode_float_batch: like qkd_decode_batch with float LLRs; final_L_dev (float [F][n_edges],
- *   canonical order) and final_E_dev (float [F][n]) optional.  Check degrees <= 20.
+ *   canonical order) and final_E_dev (float [F][n]) optional.  Check degrees <= 32.
  *   schedule 0 = layered (the paper's); 1 = flooding: every iteration all
  *   check nodes from the previous state, then E_j = LLR_j + sum_i L_ij (float atomics, so the
  *   summation order -- and the last bits of E -- vary from run to run).

@@ -15,7 +15,7 @@
 
 namespace qkd {
 
-constexpr int kFloatDMax = 20;          // check degrees handled by the float kernel
+constexpr int kFloatDMax = 32;          // check degrees handled by the float kernel (instances FD = 20, 32)
 constexpr float kLlrKnown = 1000.0f;    // R26
 
 struct FParams {
@@ -49,13 +49,14 @@ __device__ __forceinline__ int col_f(const int2 e, int r, int Z) {
     return e.x + idx;
 }
 
-// one check row r of a block row (degree D <= kFloatDMax)
+// one check row r of a block row (degree D <= FD)
+template <int FD>
 __device__ __forceinline__ void row_update_f(const int2* __restrict__ et, int D, int Z, int r, float* E,
                                              float* __restrict__ Lrow, int s_i, bool first) {
-    float x[kFloatDMax], mg[kFloatDMax], o[kFloatDMax];
+    float x[FD], mg[FD], o[FD];
     int sg = s_i, neg = 0;
 #pragma unroll
-    for (int k = 0; k < kFloatDMax; ++k) {
+    for (int k = 0; k < FD; ++k) {
         if (k < D) {
             const float xv = E[col_f(et[k], r, Z)] - (first ? 0.0f : Lrow[k]);   // Eq.(8)
             x[k] = xv;
@@ -69,15 +70,15 @@ __device__ __forceinline__ void row_update_f(const int2* __restrict__ et, int D,
         o[0] = kLlrKnown;                                  // empty box-plus (R26)
     } else {
         // forward chain F_k in o[k+1] scratch, backward chain accumulated in b; o_k = beta(F_{k-1}, B_{k+1})
-        float F[kFloatDMax];
+        float F[FD];
         F[0] = mg[0];
 #pragma unroll
-        for (int k = 1; k < kFloatDMax; ++k)
+        for (int k = 1; k < FD; ++k)
             if (k < D - 1) F[k] = beta_f(F[k - 1], mg[k]);
         float b = mg[D - 1];
         o[D - 1] = F[D - 2];
 #pragma unroll
-        for (int k = kFloatDMax - 2; k >= 1; --k) {
+        for (int k = FD - 2; k >= 1; --k) {
             if (k <= D - 2) {
                 o[k] = beta_f(F[k - 1], b);
                 b = beta_f(mg[k], b);
@@ -86,7 +87,7 @@ __device__ __forceinline__ void row_update_f(const int2* __restrict__ et, int D,
         o[0] = b;
     }
 #pragma unroll
-    for (int k = 0; k < kFloatDMax; ++k) {
+    for (int k = 0; k < FD; ++k) {
         if (k < D) {
             const float ln = ((sg ^ (neg >> k)) & 1) ? -o[k] : o[k];     // Eq.(1)
             Lrow[k] = ln;
@@ -98,12 +99,13 @@ __device__ __forceinline__ void row_update_f(const int2* __restrict__ et, int D,
 // Flooding schedule: the check-node half of an iteration -- every row from the
 // previous iteration's E and L (Eq.(8)), L_new stored; E is left untouched (the variable-node half,
 // E_j = LLR_j + sum_i L_ij, runs after a barrier).
+template <int FD>
 __device__ __forceinline__ void row_check_f(const int2* __restrict__ et, int D, int Z, int r, const float* E,
                                             float* __restrict__ Lrow, int s_i, bool first) {
-    float mg[kFloatDMax], o[kFloatDMax];
+    float mg[FD], o[FD];
     int sg = s_i, neg = 0;
 #pragma unroll
-    for (int k = 0; k < kFloatDMax; ++k) {
+    for (int k = 0; k < FD; ++k) {
         if (k < D) {
             const float xv = E[col_f(et[k], r, Z)] - (first ? 0.0f : Lrow[k]);
             mg[k] = fabsf(xv);
@@ -115,15 +117,15 @@ __device__ __forceinline__ void row_check_f(const int2* __restrict__ et, int D, 
     if (D == 1) {
         o[0] = kLlrKnown;
     } else {
-        float F[kFloatDMax];
+        float F[FD];
         F[0] = mg[0];
 #pragma unroll
-        for (int k = 1; k < kFloatDMax; ++k)
+        for (int k = 1; k < FD; ++k)
             if (k < D - 1) F[k] = beta_f(F[k - 1], mg[k]);
         float b = mg[D - 1];
         o[D - 1] = F[D - 2];
 #pragma unroll
-        for (int k = kFloatDMax - 2; k >= 1; --k) {
+        for (int k = FD - 2; k >= 1; --k) {
             if (k <= D - 2) {
                 o[k] = beta_f(F[k - 1], b);
                 b = beta_f(mg[k], b);
@@ -132,7 +134,7 @@ __device__ __forceinline__ void row_check_f(const int2* __restrict__ et, int D, 
         o[0] = b;
     }
 #pragma unroll
-    for (int k = 0; k < kFloatDMax; ++k)
+    for (int k = 0; k < FD; ++k)
         if (k < D) Lrow[k] = ((sg ^ (neg >> k)) & 1) ? -o[k] : o[k];
 }
 

@@ -758,7 +758,7 @@ __global__ void scatter_results_kernel(const int32_t* __restrict__ idx, long lon
 // --------------------------------------------------------------------------------------
 // exact floating-point layered BP (decode_float.cuh): one frame per slot
 // --------------------------------------------------------------------------------------
-template <bool ESM, bool FLOOD>
+template <bool ESM, bool FLOOD, int FD>
 __global__ void __launch_bounds__(1024, 1) decode_float_kernel(const FParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     int4* s_layer = reinterpret_cast<int4*>(smem + p.tab_off);
@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(1024, 1) decode_float_kernel(const FParams p) 
                 for (int I = 0; I < p.Mb; ++I) {
                     const int4 li = s_layer[I];
                     for (int r = t; r < p.Z; r += p.TG)
-                        row_update_f(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
+                        row_update_f<FD>(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
                                      sSyn[I * p.Z + r], it == 1);
                     group_bar(bar, p.TG);
                 }
@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(1024, 1) decode_float_kernel(const FParams p) 
                 for (int I = 0; I < p.Mb; ++I) {
                     const int4 li = s_layer[I];
                     for (int r = t; r < p.Z; r += p.TG)
-                        row_check_f(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
+                        row_check_f<FD>(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
                                     sSyn[I * p.Z + r], it == 1);
                 }
                 group_bar(bar, p.TG);
@@ -1461,13 +1461,26 @@ int qkd_reconcile_adaptive(const qkd_code* c, double qber, int64_t F, const int3
 // ---- exact floating-point BP ---------------------------------------
 struct FPlan {
     bool esm = false;
+    int fd = 20;   // register-array size of the row update: 20 or 32 (kFloatDMax)
     int TG = 0, GPC = 0, grid = 0, smem = 0, slot_bytes = 0, e_bytes = 0, tab_off = 0;
     long long slots = 0;
     size_t ws_total = 0;
 };
 
+static const void* fkernel(bool esm, bool flood, int fd) {
+    if (fd <= 20)
+        return esm ? (flood ? reinterpret_cast<const void*>(&decode_float_kernel<true, true, 20>)
+                            : reinterpret_cast<const void*>(&decode_float_kernel<true, false, 20>))
+                   : (flood ? reinterpret_cast<const void*>(&decode_float_kernel<false, true, 20>)
+                            : reinterpret_cast<const void*>(&decode_float_kernel<false, false, 20>));
+    return esm ? (flood ? reinterpret_cast<const void*>(&decode_float_kernel<true, true, kFloatDMax>)
+                        : reinterpret_cast<const void*>(&decode_float_kernel<true, false, kFloatDMax>))
+               : (flood ? reinterpret_cast<const void*>(&decode_float_kernel<false, true, kFloatDMax>)
+                        : reinterpret_cast<const void*>(&decode_float_kernel<false, false, kFloatDMax>));
+}
+
 static int make_fplan(const qkd_code* c, long long F, FPlan& pl) {
-    if (c->maxdeg > kFloatDMax) return fail(QKD_EUNSUP, "float decoder: check degree > 20");
+    if (c->maxdeg > kFloatDMax) return fail(QKD_EUNSUP, "float decoder: check degree > 32");
     int dev = 0;
     QKD_CK(cudaGetDevice(&dev));
     const DevInfo di = dev_info(dev);
@@ -1485,13 +1498,11 @@ static int make_fplan(const qkd_code* c, long long F, FPlan& pl) {
     pl.GPC = gpc;
     pl.tab_off = gpc * pl.slot_bytes;
     pl.smem = pl.tab_off + (int)tab;
-    for (const void* k : {reinterpret_cast<const void*>(&decode_float_kernel<true, false>),
-                          reinterpret_cast<const void*>(&decode_float_kernel<true, true>),
-                          reinterpret_cast<const void*>(&decode_float_kernel<false, false>),
-                          reinterpret_cast<const void*>(&decode_float_kernel<false, true>)})
+    pl.fd = c->maxdeg <= 20 ? 20 : kFloatDMax;
+    for (const void* k : {fkernel(true, false, pl.fd), fkernel(true, true, pl.fd), fkernel(false, false, pl.fd),
+                          fkernel(false, true, pl.fd)})
         QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
-    const void* k = pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true, false>)
-                           : reinterpret_cast<const void*>(&decode_float_kernel<false, false>);
+    const void* k = fkernel(pl.esm, false, pl.fd);
     int per_sm = 0;
     QKD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.TG * pl.GPC, pl.smem));
     if (per_sm < 1) return fail(QKD_EUNSUP, "float decoder cannot be resident with this geometry");
@@ -1568,10 +1579,7 @@ int qkd_decode_float_batch(const qkd_code* c, int64_t F, const float* llr, const
     cudaStream_t st = (cudaStream_t)stream;
     QKD_CK(cudaMemsetAsync(p.work, 0, sizeof(int), st));
     void* args[] = {&p};
-    const void* k = schedule ? (pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true, true>)
-                                       : reinterpret_cast<const void*>(&decode_float_kernel<false, true>))
-                             : (pl.esm ? reinterpret_cast<const void*>(&decode_float_kernel<true, false>)
-                                       : reinterpret_cast<const void*>(&decode_float_kernel<false, false>));
+    const void* k = fkernel(pl.esm, schedule != 0, pl.fd);
     QKD_CK(cudaLaunchKernel(k, dim3(pl.grid), dim3(pl.TG * pl.GPC), args, pl.smem, st));
     QKD_CK(cudaGetLastError());
     return QKD_OK;

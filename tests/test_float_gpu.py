@@ -97,3 +97,25 @@ def test_flooding_full_decodes(gpu):
     g = {k: v.cpu().numpy() for k, v in g.items()}
     same = (g["iters"] == o["iters"]) & (g["success"] == o["success"]) & (g["bits"] == o["bits"]).all(axis=1)
     assert same.mean() >= 0.95, same.mean()
+
+
+@pytest.mark.parametrize("flooding", [False, True])
+def test_float_degree_21_to_32(gpu, flooding):
+    """The FD = 32 instance of the float kernel (check degrees 21..32): the N3 stable-profile code
+    (check degree 27-28) at QBER 1.75 %, a few sweeps against the fp64 oracle."""
+    import torch
+
+    cols = [8] * 16 + [3] * 21 + [2] * 13
+    shifts = synth.girth6_shifts(synth.peg_mask(8, cols, 7), 1024, 8)
+    oc = oracle.Code(shifts, 1024)
+    x, y, _ = synth.frames(oc.n, 0.0175, 203, 0, 2)
+    syn = oc.syndrome(x)
+    llr_o = oracle.build_llr_float(oc.n, 0.0175, y)
+    code = gpu.QCCode(shifts, 1024)
+    llr_g = code.build_llr_float(0.0175, torch.from_numpy(y).cuda())
+    for T in (1, 3):
+        o = oracle.decode_float(oc, llr_o, syn, T, 0, flooding=flooding)
+        g = code.decode_float(llr_g, torch.from_numpy(syn).cuda(), T, False, want_state=True, flooding=flooding)
+        for k in ("E", "L"):
+            gv = g[k].cpu().numpy()
+            assert np.allclose(gv, o[k], rtol=1e-5, atol=2e-3 * T), (k, T, np.abs(gv - o[k]).max())

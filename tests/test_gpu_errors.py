@@ -45,7 +45,7 @@ def test_call_errors(gpu):
 def test_float_decoder_degree_limit(gpu):
     import torch
 
-    code = gpu.QCCode(np.zeros((1, 22), dtype=np.int32), 3)                              # check degree 22
+    code = gpu.QCCode(np.zeros((1, 34), dtype=np.int32), 3)                              # check degree 34 > 32
     F = 2
     y = torch.zeros((F, code.nb8), dtype=torch.uint8, device="cuda")
     llr = code.build_llr_float(0.05, y)

@@ -8,7 +8,8 @@ frames ("maintain the high efficiency as the floating-po
 For each (code, QBER) point: frame error rate (syndrome not matched, or matched with payload errors),
 mean iterations, and decode time of both decoders on identical BSC frames.  Codes: BASELINE configs[0]
 (C1) and configs[1] (C2) at and around their QBERs, and the C4 mother code unpunctured at 6 % and 8 %
-(SURVEY §8(d) diagnostic points, f = 1.527 / 1.243).
+(SURVEY §8(d) diagnostic points, f = 1.527 / 1.243), plus the best stable rate-0.84 profile of N3
+(profiles/r1_degree_profiles.md) at 1.5 / 1.75 / 2 % (f = 1.42 / 1.26 / 1.13).
 """
 from __future__ import annotations
 
@@ -27,10 +28,28 @@ import paper_1903_10107_b200 as qkd  # noqa: E402
 import synth  # noqa: E402
 
 POINTS = [("C1", 0.04), ("C1", 0.05), ("C1", 0.06), ("C2", 0.06), ("C2", 0.07), ("C2", 0.08), ("C2", 0.09),
-          ("C4mother", 0.06), ("C4mother", 0.08)]
+          ("C4mother", 0.06), ("C4mother", 0.08), ("N3best", 0.015), ("N3best", 0.0175), ("N3best", 0.02)]
+
+
+class _N3Best:
+    """The best stable rate-0.84 profile of profiles/r1_degree_profiles.md (n = 51200, check degree 27-28)."""
+    Z, n, max_iter = 1024, 51200, 50
+
+    def __init__(self, q):
+        self.qber = q
+        cols = [8] * 16 + [3] * 21 + [2] * 13
+        self._sh = synth.girth6_shifts(synth.peg_mask(8, cols, 7), 1024, 8)
+
+    def shifts(self):
+        return self._sh
+
+    def gen(self, f0, F):
+        return synth.frames(self.n, self.qber, 203, f0, F)
 
 
 def workload(name, q):
+    if name == "N3best":
+        return _N3Best(q)
     if name == "C4mother":
         w = synth.workload("C4@0.06")
         w.rate_adaptive = False          # unpunctured mother code (diagnostic point)
