@@ -239,7 +239,7 @@ __device__ void finalize(const DecParams& p, const int4* s_layer, const uint32_t
 }
 
 template <int DMAX, bool ESM, bool POW2, bool SPLIT, bool REFILL>
-__global__ void __launch_bounds__(SPLIT || DMAX == 8 ? 1024 : (DMAX == 20 || DMAX == 32 ? QKD_D32_TG(DMAX) : 256), 1)
+__global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 20 || DMAX == 32 || DMAX == 8 ? QKD_D32_TG(DMAX) : 256), 1)
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Konst K = p.K.in_regs();
@@ -921,7 +921,7 @@ const void* kfun() {
 
 // refill: per-frame lane scheduling (opt-in, QKD_REFILL=1; not for the lane-pair variant)
 const void* kernel_of(int variant, bool pow2, bool refill = false) {
-    if (refill && variant != 5 && variant != 6) {
+    if (refill && variant != 5 && variant != 6 && variant != 7) {
         switch (variant) {
             case 1: return pow2 ? kfun<8, true, true, false, true>() : kfun<8, true, false, false, true>();
             case 2: return pow2 ? kfun<20, true, true, false, true>() : kfun<20, true, false, false, true>();
@@ -934,6 +934,7 @@ const void* kernel_of(int variant, bool pow2, bool refill = false) {
         case 2: return pow2 ? kfun<20, true, true>() : kfun<20, true, false>();
         case 3: return kfun<0, true, false>();
         case 6: return pow2 ? kfun<32, true, true>() : kfun<32, true, false>();
+        case 7: return kfun<8, false, false>();
         case 5: return pow2 ? kfun<20, true, true, true>() : kfun<20, true, false, true>();
         default: return kfun<0, false, false>();
     }
@@ -947,6 +948,7 @@ Konst runtime_konst() {
 // Decode variant of a code on a device (fixed at code creation: the split variant has its own
 // message layout).  1: degree <= 8, smem E; 2: degree <= 20, smem E, one row per thread;
 // 5: degree 9..20, smem E, lane-pair rows; 6: degree 21..32, smem E, one row per thread;
+// 7: degree <= 8, E in global memory (frames too long for shared memory), register rows;
 // 3: generic smem E; 4: generic global E.
 int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem_optin, bool allow_split) {
     const long long syn_ctl = ((m + 15) & ~15LL) + 64;
@@ -956,6 +958,7 @@ int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem
     if (fits && maxdeg <= 8) return 1;
     if (fits && maxdeg <= 20) return allow_split ? 5 : 2;
     if (fits && maxdeg <= 32 && !std::getenv("QKD_NO_D32")) return 6;
+    if (!fits && maxdeg <= 8 && !std::getenv("QKD_NO_GREG")) return 7;
     return fits ? 3 : 4;
 }
 
@@ -969,14 +972,15 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     const long long e_bytes = 4LL * c->n;
     pl.variant = choose_variant(c->Mb, c->n, c->m, c->nbase, c->maxdeg, di.smem_optin, c->split);
     if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
-    pl.pow2 = (pl.variant <= 2 || pl.variant >= 5) && ((c->Z & (c->Z - 1)) == 0);
+    pl.pow2 = (pl.variant <= 2 || pl.variant == 5 || pl.variant == 6) && ((c->Z & (c->Z - 1)) == 0);
     const int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024
-                       : (pl.variant == 2 ? 512 : (pl.variant == 6 ? QKD_D32_THREADS : 256));
+                       : (pl.variant == 2 || pl.variant == 7 ? 512 : (pl.variant == 6 ? QKD_D32_THREADS : 256));
     if (pl.variant == 5)   // two lanes per row, 16 rows per warp
         pl.TG = (int)std::min<long long>(((long long)c->Z + 15) / 16 * 32, tg_max);
     else
         pl.TG = (int)std::min<long long>(((long long)c->Z + 31) / 32 * 32, tg_max);
-    pl.e_bytes = pl.variant == 4 ? 0 : (int)e_bytes;
+    const bool gE = pl.variant == 4 || pl.variant == 7;   // E in the global workspace
+    pl.e_bytes = gE ? 0 : (int)e_bytes;
     long long slot = (pl.e_bytes + syn_ctl + 15) & ~15LL;   // 16-byte aligned slots and tables
     if (pl.pow2) {   // slot E bases must be multiples of 4Z for the byte-OR addressing
         const long long al = 4LL * c->Z;
@@ -1005,7 +1009,7 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     pl.grid = (int)std::max<long long>(1, std::min<long long>(ctas, (long long)per_sm * di.sms));
     pl.slots = (long long)pl.grid * gpc;
     pl.ws_L = (size_t)pl.slots * (size_t)c->ws_words * 4;
-    pl.ws_E = pl.variant == 4 ? (size_t)pl.slots * (size_t)c->n * 4 : 0;
+    pl.ws_E = gE ? (size_t)pl.slots * (size_t)c->n * 4 : 0;
     pl.ws_total = 256 + pl.ws_L + pl.ws_E;
     return QKD_OK;
 }
@@ -1251,7 +1255,7 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
         // (QKD_REFILL=1; C5a +9%); QKD_REFILL=0 turns it off everywhere
         const char* env = std::getenv("QKD_REFILL");
         const bool on = env ? env[0] == '1' : pl.variant == 1;
-        p.refill = (pl.variant != 5 && pl.variant != 6 && on) ? 1 : 0;
+        p.refill = (pl.variant != 5 && pl.variant != 6 && pl.variant != 7 && on) ? 1 : 0;
     }
     p.work = reinterpret_cast<int*>(w);
     p.Lws = reinterpret_cast<uint32_t*>(w + 256);

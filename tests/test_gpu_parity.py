@@ -263,6 +263,19 @@ def test_degree32_variant_against_generic(gpu, monkeypatch, case):
     assert_same(g, o)
 
 
+@pytest.mark.parametrize("greg", ["1", "0"])
+def test_global_e_variants(gpu, monkeypatch, greg):
+    """C4 (E does not fit in shared memory, check degree <= 8): the register-row kernel with E in
+    global memory (variant 7) and, with QKD_NO_GREG=1, the generic one (variant 4)."""
+    if greg == "0":
+        monkeypatch.setenv("QKD_NO_GREG", "1")
+    w, shifts, kind, x, y, llr, syn = workload_inputs("C4@0.04", 5)
+    g, code = gpu_decode(gpu, shifts, w.Z, kind, llr, syn, 9, 0)
+    assert code.launch_info(5)["variant"] == (7 if greg == "1" else 4)
+    o = oracle_decode(shifts, w.Z, llr, syn, 9, 0)
+    assert_same(g, o)
+
+
 def test_stable_profile_code_parity(gpu):
     """The best stable degree profile of profiles/r1_degree_profiles.md (check degree 27-28, variant 6)
     on channel frames at QBER 1.75 %, bit-exact against the oracle."""
