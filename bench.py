@@ -246,7 +246,7 @@ def run_gpu(args):
     W = []
     for name in names:
         w = synth.workload(name)
-        F = w.frames
+        F = w.frames * (world if args.scaling == "weak" else 1)   # weak: BASELINE's count on every rank
         a, b = shard(F, rank, world)
         t0 = time.perf_counter()
         x, y, _ = w.gen(a, b - a, nthreads)
@@ -378,8 +378,9 @@ def run_gpu(args):
             cpu["single_thread_sample"] = ", ".join(f"first {per1[n]} frames of {n}" for n in names)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "int8", "data": "synthetic",
                 "config": dict(workload_config(args.workload), parallelism=f"frames sharded over {world} rank(s)",
+                               frames_total={s["name"]: int(c[i, 0]) for i, s in enumerate(W)},
                                processed_key_mbps=processed, per_workload=per_wl),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic, "ncu": ncu,
@@ -455,6 +456,9 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default, BASELINE configs[4]: 65536 frames per workload in total, split "
+                         "across ranks) or weak (65536 frames per workload on every rank)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")
