@@ -973,8 +973,10 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     pl.variant = choose_variant(c->Mb, c->n, c->m, c->nbase, c->maxdeg, di.smem_optin, c->split);
     if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
     pl.pow2 = (pl.variant <= 2 || pl.variant == 5 || pl.variant == 6) && ((c->Z & (c->Z - 1)) == 0);
-    const int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024
-                       : (pl.variant == 2 || pl.variant == 7 ? 512 : (pl.variant == 6 ? QKD_D32_THREADS : 256));
+    int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024
+                 : (pl.variant == 2 || pl.variant == 7 ? 512 : (pl.variant == 6 ? QKD_D32_THREADS : 256));
+    if (const char* e = std::getenv("QKD_TG_MAX"))   // experiments: fewer threads per frame group
+        tg_max = std::max(32, std::min(tg_max, atoi(e) / 32 * 32));
     if (pl.variant == 5)   // two lanes per row, 16 rows per warp
         pl.TG = (int)std::min<long long>(((long long)c->Z + 15) / 16 * 32, tg_max);
     else
