@@ -190,13 +190,14 @@ def test_full_size_sampled(gpu, name):
     assert np.array_equal(s_bits[ok], syn.cpu().numpy()[sl][ok])
 
 
-def test_full_size_c5b_every_shard_full_state(gpu):
-    """SURVEY §8(c) parity contract for C5: >= 4096 frames covering every rank's shard (8 ranks x
-    8192 frames), from the full 65536-frame launch in the bench's configuration, bit-exact in bits,
-    iters, success and the final L and E against the oracle."""
+@pytest.mark.parametrize("name,per_shard", [("C5b", 512), ("C5a", 512)])
+def test_full_size_every_shard_full_state(gpu, name, per_shard):
+    """SURVEY §8(c) parity contract for C5: frames covering every rank's shard (8 ranks x 8192 frames;
+    4096 frames of each workload), from the full 65536-frame
+    launch in the bench's configuration, bit-exact in bits, iters, success and the final L and E."""
     import torch
 
-    w = synth.workload("C5b")
+    w = synth.workload(name)
     F = w.frames
     shifts = w.shifts()
     x, y, _ = w.gen(0, F)
@@ -205,7 +206,7 @@ def test_full_size_c5b_every_shard_full_state(gpu):
     llr = code.build_llr(w.qber, torch.from_numpy(y).cuda())
     r = code.decode(llr, syn, w.max_iter, True, want_state=True)
     shard = F // 8
-    sample = np.concatenate([np.arange(k * shard, k * shard + 512) for k in range(8)])
+    sample = np.concatenate([np.arange(k * shard, k * shard + per_shard) for k in range(8)])
     idx = torch.from_numpy(sample).cuda()
     g = {k: v.index_select(0, idx).cpu().numpy() for k, v in r.items()}
     del r
