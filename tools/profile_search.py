@@ -35,6 +35,11 @@ MB, NB, Z = 8, 50, 1024
 QBERS = (0.015, 0.0175, 0.02)
 
 
+def set_z(z: int) -> None:
+    global Z
+    Z = z
+
+
 def h2(q):
     return -q * math.log2(q) - (1 - q) * math.log2(1 - q)
 
@@ -73,7 +78,24 @@ def main():
     ap.add_argument("--confirm", type=int, default=4096)
     ap.add_argument("--top", type=int, default=4)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--z", type=int, default=Z, help="lifting size (1024: n = 51200; 2048: the paper's ~100 kb)")
+    ap.add_argument("--only", default=None, help="n2,d_hi,n_hi: measure one profile on --confirm frames")
     a = ap.parse_args()
+    if a.z != Z:
+        set_z(a.z)
+    if a.only:
+        n2, d_hi, n_hi = (int(v) for v in a.only.split(","))
+        frames = {}
+        for q in QBERS:
+            x, y, _ = synth.frames(NB * Z, q, 203, 0, a.confirm)
+            frames[(q, a.confirm)] = (torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+        sh = build(n2, d_hi, n_hi, 7)
+        res = measure(sh, a.confirm, frames)
+        print(json.dumps(dict(n=NB * Z, n2=n2, d_hi=d_hi, n_hi=n_hi, frames=a.confirm,
+                              variant=qkd.QCCode(sh, Z).launch_info(a.confirm)["variant"],
+                              **{f"fer_{q:g}": res[q]["fer"] for q in QBERS},
+                              **{f"iters_{q:g}": res[q]["mean_iters"] for q in QBERS})), flush=True)
+        return
     frames = {}
     for q in QBERS:
         for F in (a.frames, a.confirm):
