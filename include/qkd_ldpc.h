@@ -194,7 +194,7 @@ int qkd_decode_float_batch(const qkd_code* code, int64_t n_frames, const float* 
  * info[0] kernel variant (1: degree<=8 smem, 2: degree<=20 smem, 3: generic smem,
  * 4: generic with E in global memory, 5: degree 9..20 lane-pair rows (QKD_SPLIT=1 at
  * code creation), 6: degree 21..32 smem, one row per thread, 7: degree <= 8 with E in global memory,
- * register rows; +10 when Z is a power of two), [1] threads per frame group, [2] frame groups per
+ * register rows, 8: degree 9..32 with E in global memory, register rows; +10 when Z is a power of two), [1] threads per frame group, [2] frame groups per
  * CTA, [3] grid, [4] dynamic shared bytes per CTA, [5] frames per group (4), [6] groups. */
 int qkd_launch_info(const qkd_code* code, int64_t n_frames, int32_t* info);
 

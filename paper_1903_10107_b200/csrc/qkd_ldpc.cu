@@ -921,7 +921,7 @@ const void* kfun() {
 
 // refill: per-frame lane scheduling (opt-in, QKD_REFILL=1; not for the lane-pair variant)
 const void* kernel_of(int variant, bool pow2, bool refill = false) {
-    if (refill && variant != 5 && variant != 6 && variant != 7) {
+    if (refill && variant != 5 && variant < 6) {
         switch (variant) {
             case 1: return pow2 ? kfun<8, true, true, false, true>() : kfun<8, true, false, false, true>();
             case 2: return pow2 ? kfun<20, true, true, false, true>() : kfun<20, true, false, false, true>();
@@ -935,6 +935,7 @@ const void* kernel_of(int variant, bool pow2, bool refill = false) {
         case 3: return kfun<0, true, false>();
         case 6: return pow2 ? kfun<32, true, true>() : kfun<32, true, false>();
         case 7: return kfun<8, false, false>();
+        case 8: return kfun<32, false, false>();
         case 5: return pow2 ? kfun<20, true, true, true>() : kfun<20, true, false, true>();
         default: return kfun<0, false, false>();
     }
@@ -949,6 +950,7 @@ Konst runtime_konst() {
 // message layout).  1: degree <= 8, smem E; 2: degree <= 20, smem E, one row per thread;
 // 5: degree 9..20, smem E, lane-pair rows; 6: degree 21..32, smem E, one row per thread;
 // 7: degree <= 8, E in global memory (frames too long for shared memory), register rows;
+// 8: degree 9..32, E in global memory, register rows;
 // 3: generic smem E; 4: generic global E.
 int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem_optin, bool allow_split) {
     const long long syn_ctl = ((m + 15) & ~15LL) + 64;
@@ -958,7 +960,7 @@ int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem
     if (fits && maxdeg <= 8) return 1;
     if (fits && maxdeg <= 20) return allow_split ? 5 : 2;
     if (fits && maxdeg <= 32 && !std::getenv("QKD_NO_D32")) return 6;
-    if (!fits && maxdeg <= 8 && !std::getenv("QKD_NO_GREG")) return 7;
+    if (!fits && maxdeg <= 32 && !std::getenv("QKD_NO_GREG")) return maxdeg <= 8 ? 7 : 8;
     return fits ? 3 : 4;
 }
 
@@ -972,16 +974,16 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     const long long e_bytes = 4LL * c->n;
     pl.variant = choose_variant(c->Mb, c->n, c->m, c->nbase, c->maxdeg, di.smem_optin, c->split);
     if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
-    pl.pow2 = (pl.variant <= 2 || pl.variant == 5 || pl.variant == 6) && ((c->Z & (c->Z - 1)) == 0);
+    pl.pow2 = (pl.variant <= 2 || pl.variant == 5 || pl.variant == 6) && ((c->Z & (c->Z - 1)) == 0);   // smem E only
     int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024
-                 : (pl.variant == 2 || pl.variant == 7 ? 512 : (pl.variant == 6 ? QKD_D32_THREADS : 256));
+                 : (pl.variant == 2 || pl.variant == 7 ? 512 : (pl.variant >= 6 ? QKD_D32_THREADS : 256));
     if (const char* e = std::getenv("QKD_TG_MAX"))   // experiments: fewer threads per frame group
         tg_max = std::max(32, std::min(tg_max, atoi(e) / 32 * 32));
     if (pl.variant == 5)   // two lanes per row, 16 rows per warp
         pl.TG = (int)std::min<long long>(((long long)c->Z + 15) / 16 * 32, tg_max);
     else
         pl.TG = (int)std::min<long long>(((long long)c->Z + 31) / 32 * 32, tg_max);
-    const bool gE = pl.variant == 4 || pl.variant == 7;   // E in the global workspace
+    const bool gE = pl.variant == 4 || pl.variant >= 7;   // E in the global workspace
     pl.e_bytes = gE ? 0 : (int)e_bytes;
     long long slot = (pl.e_bytes + syn_ctl + 15) & ~15LL;   // 16-byte aligned slots and tables
     if (pl.pow2) {   // slot E bases must be multiples of 4Z for the byte-OR addressing
@@ -1257,7 +1259,7 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
         // (QKD_REFILL=1; C5a +9%); QKD_REFILL=0 turns it off everywhere
         const char* env = std::getenv("QKD_REFILL");
         const bool on = env ? env[0] == '1' : pl.variant == 1;
-        p.refill = (pl.variant != 5 && pl.variant != 6 && pl.variant != 7 && on) ? 1 : 0;
+        p.refill = (pl.variant != 5 && pl.variant < 6 && on) ? 1 : 0;
     }
     p.work = reinterpret_cast<int*>(w);
     p.Lws = reinterpret_cast<uint32_t*>(w + 256);

@@ -277,6 +277,25 @@ def test_global_e_variants(gpu, monkeypatch, greg):
     assert_same(g, o)
 
 
+@pytest.mark.parametrize("greg", ["1", "0"])
+def test_global_e_high_degree_variant(gpu, monkeypatch, greg):
+    """The N3 stable profile lifted to the paper's ~100 kb frames (n = 102400, check degree 27-28: E does
+    not fit in shared memory): register rows with E in global memory (variant 8) and, with
+    QKD_NO_GREG=1, the generic kernel (variant 4), on channel frames at 1.75 %."""
+    if greg == "0":
+        monkeypatch.setenv("QKD_NO_GREG", "1")
+    cols = [8] * 16 + [3] * 21 + [2] * 13
+    shifts = synth.girth6_shifts(synth.peg_mask(8, cols, 7), 2048, 8)
+    oc = oracle.Code(shifts, 2048)
+    x, y, _ = synth.frames(oc.n, 0.0175, 203, 0, 5)
+    syn = oc.syndrome(x)
+    llr = oc.build_llr(0.0175, y)
+    g, code = gpu_decode(gpu, shifts, 2048, None, llr, syn, 50, 1)
+    assert code.launch_info(5)["variant"] == (8 if greg == "1" else 4)
+    o = oracle_decode(shifts, 2048, llr, syn, 50, 1)
+    assert_same(g, o)
+
+
 def test_stable_profile_code_parity(gpu):
     """The best stable degree profile of profiles/r1_degree_profiles.md (check degree 27-28, variant 6)
     on channel frames at QBER 1.75 %, bit-exact against the oracle."""
