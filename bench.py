@@ -343,6 +343,8 @@ def run_gpu(args):
     try:   # from the committed ncu capture of this launch (profiles/<tag>_decode_full.md)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
+        if tj.get("workload", "C5a") != dom:   # the capture is of another workload's launch
+            raise LookupError
         traffic = tj.get("decode_dram_bytes_per_launch")
         ncu = dict(tj.get("ncu") or {}, source=tj.get("source"))
         if world > 1:   # the capture is of the 1-GPU launch (all frames of the workload)

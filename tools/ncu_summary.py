@@ -79,6 +79,7 @@ def main():
     ap.add_argument("--full")
     ap.add_argument("--algo-bytes", type=float, default=None, help="algorithmic bytes of the first decode launch")
     ap.add_argument("--note", default="")
+    ap.add_argument("--workload", default="C5a", help="workload of the captured decode launch (bench.py matches it)")
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
@@ -143,7 +144,8 @@ def main():
         }
         with open(os.path.join(prof, "traffic.json"), "w") as f:
             json.dump({"decode_dram_bytes_per_launch": dram, "ncu": counters,
-                       "source": f"profiles/{a.tag}_decode_full.md", "kernel": first["kernel"]}, f, indent=1)
+                       "source": f"profiles/{a.tag}_decode_full.md", "kernel": first["kernel"],
+                       "workload": a.workload}, f, indent=1)
         print("\n".join(lines))
 
 
