@@ -80,6 +80,7 @@ def main():
     ap.add_argument("--algo-bytes", type=float, default=None, help="algorithmic bytes of the first decode launch")
     ap.add_argument("--note", default="")
     ap.add_argument("--workload", default="C5a", help="workload of the captured decode launch (bench.py matches it)")
+    ap.add_argument("--no-traffic", action="store_true", help="do not rewrite profiles/traffic.json")
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
@@ -142,10 +143,11 @@ def main():
             "warp_instructions": num("smsp__inst_executed.sum"),
             "duration_ms_under_ncu": dur_ms,
         }
-        with open(os.path.join(prof, "traffic.json"), "w") as f:
-            json.dump({"decode_dram_bytes_per_launch": dram, "ncu": counters,
-                       "source": f"profiles/{a.tag}_decode_full.md", "kernel": first["kernel"],
-                       "workload": a.workload}, f, indent=1)
+        if not a.no_traffic:
+            with open(os.path.join(prof, "traffic.json"), "w") as f:
+                json.dump({"decode_dram_bytes_per_launch": dram, "ncu": counters,
+                           "source": f"profiles/{a.tag}_decode_full.md", "kernel": first["kernel"],
+                           "workload": a.workload}, f, indent=1)
         print("\n".join(lines))
 
 
