@@ -76,6 +76,7 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
                                            const Konst& K) {
     const bool first = fresh == 0xFu;   // all four lanes on their first sweep: L = 0 without loading
     const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
+    if (li.x == 0) return;              // a check row with no variables: nothing to update (oracle: no-op)
     if constexpr (SPLIT) {
         // lane pairs: warp-uniform trip count (the shuffles need all 32 lanes), 16 rows per warp pass
         const int side = t & 1, pairs = p.TG >> 1, wa = ((li.x >> 1) + 1) & ~1;
@@ -812,7 +813,7 @@ __global__ void __launch_bounds__(1024, 1) decode_float_kernel(const FParams p) 
             if constexpr (!FLOOD) {   // layered: each block row sees the previous ones' E
                 for (int I = 0; I < p.Mb; ++I) {
                     const int4 li = s_layer[I];
-                    for (int r = t; r < p.Z; r += p.TG)
+                    for (int r = t; r < p.Z && li.x > 0; r += p.TG)
                         row_update_f<FD>(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
                                      sSyn[I * p.Z + r], it == 1);
                     group_bar(bar, p.TG);
@@ -820,7 +821,7 @@ __global__ void __launch_bounds__(1024, 1) decode_float_kernel(const FParams p) 
             } else {                  // flooding (N4): all checks from the old state, then all VNs
                 for (int I = 0; I < p.Mb; ++I) {
                     const int4 li = s_layer[I];
-                    for (int r = t; r < p.Z; r += p.TG)
+                    for (int r = t; r < p.Z && li.x > 0; r += p.TG)
                         row_check_f<FD>(s_edge + li.y, li.x, p.Z, r, E, Ls + li.z + (long long)r * li.w,
                                     sSyn[I * p.Z + r], it == 1);
                 }

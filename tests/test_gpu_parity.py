@@ -69,6 +69,7 @@ def _tiny_cases():
     sh[0, :4] = -1
     sh[1, :4] = rng.integers(0, 8, 4)
     cases["deg40_generic"] = (sh, 8)                                               # degree > 32
+    cases["empty_row"] = (np.array([[0, 2, -1, 1], [-1, -1, -1, -1], [3, -1, 0, 2]]), 32)   # a degree-0 block row
     return cases
 
 
