@@ -44,3 +44,48 @@ def test_random_codes(gpu, seed):
     g, code = gpu_decode(gpu, shifts, Z, None, llr, syn, T, early)
     o = oracle_decode(shifts, Z, llr, syn, T, early)
     assert_same(g, o)
+
+
+def _frames(shifts, Z, seed, F=None):
+    Mb, Nb = shifts.shape
+    n, m = Nb * Z, Mb * Z
+    rng = np.random.default_rng(zlib.crc32(f"fuzz-frames/{seed}".encode()))
+    F = F or int(rng.integers(1, 11))
+    base = np.where(rng.random((F, n)) < 0.03, -1, 1) * int(rng.choice([10, 16]))
+    wild = rng.integers(-127, 128, size=(F, n))
+    llr = np.where(rng.random((F, n)) < 0.2, wild, base).astype(np.int8)
+    syn = rng.integers(0, 256, size=(F, (m + 7) // 8), dtype=np.uint8)
+    return llr, syn
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_long_codes(gpu, seed):
+    """Frames too long for shared memory (n >= 60000): the global-E variants 7 / 8 / 4."""
+    rng = np.random.default_rng(5000 + seed)
+    Mb = int(rng.integers(1, 4))
+    Z = int(rng.choice([1536, 2048, 3001]))
+    Nb = int(max(Mb + 1, -(-60000 // Z) + int(rng.integers(0, 6))))
+    density = float(rng.choice([0.3, 0.7, 1.0]))
+    sh = np.where(rng.random((Mb, Nb)) < density, rng.integers(0, Z, (Mb, Nb)), -1)
+    for J in range(Nb):
+        if (sh[:, J] < 0).all():
+            sh[int(rng.integers(0, Mb)), J] = int(rng.integers(0, Z))
+    sh = sh.astype(np.int32)
+    llr, syn = _frames(sh, Z, 5000 + seed, F=3)
+    g, code = gpu_decode(gpu, sh, Z, None, llr, syn, 6, seed % 2)
+    assert code.launch_info(3)["variant"] in (4, 7, 8)
+    o = oracle_decode(sh, Z, llr, syn, 6, seed % 2)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("mode", ["split", "refill"])
+@pytest.mark.parametrize("seed", [2, 6, 12, 14, 15, 18, 20])
+def test_random_codes_opt_in_variants(gpu, monkeypatch, mode, seed):
+    """The opt-in scheduling variants on the random codes: lane-pair rows (QKD_SPLIT=1, degrees
+    9..20) and per-frame lane refill forced on every variant (QKD_REFILL=1)."""
+    monkeypatch.setenv("QKD_SPLIT" if mode == "split" else "QKD_REFILL", "1")
+    shifts, Z = _random_code(1000 + seed)
+    llr, syn = _frames(shifts, Z, seed, F=7)
+    g, _ = gpu_decode(gpu, shifts, Z, None, llr, syn, 9, 1)
+    o = oracle_decode(shifts, Z, llr, syn, 9, 1)
+    assert_same(g, o)
