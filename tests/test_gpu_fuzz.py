@@ -89,3 +89,66 @@ def test_random_codes_opt_in_variants(gpu, monkeypatch, mode, seed):
     g, _ = gpu_decode(gpu, shifts, Z, None, llr, syn, 9, 1)
     o = oracle_decode(shifts, Z, llr, syn, 9, 1)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_syndrome_llr_score(gpu, seed):
+    """Alice's syndrome (QC funnel-shift kernel when Z % 32 == 0, per-bit kernel otherwise), Bob's LLRs
+    with random punctured/shortened patterns and known bits, and the error score, on the random codes."""
+    import torch
+
+    import oracle
+
+    shifts, Z = _random_code(1000 + seed)
+    Mb, Nb = shifts.shape
+    n = Nb * Z
+    rng = np.random.default_rng(zlib.crc32(f"fuzz-io/{seed}".encode()))
+    F = int(rng.integers(1, 40))
+    nb8 = (n + 7) // 8
+    x = rng.integers(0, 256, size=(F, nb8), dtype=np.uint8)
+    y = rng.integers(0, 256, size=(F, nb8), dtype=np.uint8)
+    if n % 8:                                    # bits past n are zero in the packed inputs
+        x[:, -1] &= (1 << (n % 8)) - 1
+        y[:, -1] &= (1 << (n % 8)) - 1
+    kind = rng.choice(np.array([0, 0, 0, 1, 2], dtype=np.uint8), size=n) if seed % 2 else None
+    q = float(rng.choice([0.01, 0.03, 0.08, 0.2]))
+    oc = oracle.Code(shifts, Z)
+    code = gpu.QCCode(shifts, Z, kind)
+    xs, ys = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    assert np.array_equal(code.syndrome(xs).cpu().numpy(), oc.syndrome(x))
+    llr = code.build_llr(q, ys, xs if kind is not None else None).cpu().numpy()
+    assert np.array_equal(llr, oc.build_llr(q, y, kind, x if kind is not None else None))
+    succ = torch.from_numpy(rng.integers(0, 2, F).astype(np.uint8)).cuda()
+    errs = code.score(ys, xs, succ, want_errors=True).cpu().numpy()
+    diff = np.unpackbits(x ^ y, axis=1, bitorder="little")[:, :n]
+    if kind is not None:
+        diff = diff[:, kind == 0]
+    assert np.array_equal(errs, diff.sum(axis=1))
+
+
+@pytest.mark.parametrize("flooding", [False, True])
+@pytest.mark.parametrize("seed", [0, 2, 5, 8, 9, 12, 13, 16, 21])
+def test_random_codes_float(gpu, seed, flooding):
+    """Exact float BP (degrees <= 32) on the random codes: two sweeps of state against the fp64 oracle
+    within the tolerance of tests/test_float_gpu.py."""
+    import torch
+
+    import oracle
+
+    shifts, Z = _random_code(1000 + seed)
+    if (shifts >= 0).sum(axis=1).max() > 32:
+        pytest.skip("float decoder: check degree > 32")
+    oc = oracle.Code(shifts, Z)
+    rng = np.random.default_rng(zlib.crc32(f"fuzz-float/{seed}".encode()))
+    F = 3
+    y = rng.integers(0, 256, size=(F, (oc.n + 7) // 8), dtype=np.uint8)
+    syn = rng.integers(0, 256, size=(F, (oc.m + 7) // 8), dtype=np.uint8)
+    llr_o = oracle.build_llr_float(oc.n, 0.05, y)
+    code = gpu.QCCode(shifts, Z)
+    llr_g = code.build_llr_float(0.05, torch.from_numpy(y).cuda())
+    for T in (1, 2):
+        o = oracle.decode_float(oc, llr_o, syn, T, 0, flooding=flooding)
+        g = code.decode_float(llr_g, torch.from_numpy(syn).cuda(), T, False, want_state=True, flooding=flooding)
+        for k in ("E", "L"):
+            gv = g[k].cpu().numpy()
+            assert np.allclose(gv, o[k], rtol=1e-5, atol=2e-3 * T), (k, T, np.abs(gv - o[k]).max())
