@@ -54,22 +54,39 @@ def cuda_sources() -> list[str]:
     return srcs
 
 
-def build_cuda(force: bool = False, extra: list[str] | None = None) -> str:
+def build_cuda(force: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
+    """Compile every .cu of csrc/ to an object in parallel (the decode kernel variants are spread over
+    several translation units), then link the shared library."""
     srcs = cuda_sources()
-    out = os.path.join(ROOT, "paper_1903_10107_b200", "libqkdldpc.so")
-    if force or extra or _stale(out, srcs + [__file__]):
-        cu = [s for s in srcs if s.endswith(".cu")]
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-               "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-o", out, *cu]
-        if extra:
-            cmd[1:1] = extra
-        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)
-        log = os.path.join(ROOT, "paper_1903_10107_b200", "ptxas.log")
-        with open(log, "w") as f:
-            f.write(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("nvcc build failed")
+    out = out or os.path.join(ROOT, "paper_1903_10107_b200", "libqkdldpc.so")
+    if not (force or extra or _stale(out, srcs + [__file__])):
+        return out
+    cu = [s for s in srcs if s.endswith(".cu")]
+    objdir = os.path.join(os.path.dirname(out), "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    common = [NVCC, *(extra or []), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+    jobs = []
+    for src in cu:
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        jobs.append((src, obj, subprocess.Popen([*common, "-c", "-o", obj, src], cwd=ROOT,
+                                                stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    logs, failed = [], []
+    for src, obj, proc in jobs:
+        text = proc.communicate()[0]
+        logs.append(f"==== {os.path.basename(src)}\n{text}")
+        if proc.returncode != 0:
+            failed.append(src)
+    with open(os.path.join(ROOT, "paper_1903_10107_b200", "ptxas.log"), "w") as f:
+        f.write("\n".join(logs))
+    if failed:
+        sys.stderr.write("\n".join(logs))
+        raise RuntimeError("nvcc build failed: " + ", ".join(failed))
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", out, *[o for _, o, _ in jobs]], cwd=ROOT,
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed")
     return out
 
 

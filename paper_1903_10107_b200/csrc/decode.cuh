@@ -42,6 +42,16 @@ struct DecParams {
     Konst K;
 };
 
+constexpr int kFramesPerGroup = 4;   // frames per SWAR word (one byte lane each)
+
+#ifndef QKD_KEEP_ADDR
+#define QKD_KEEP_ADDR 10   // rows of degree <= this keep their E addresses in registers
+#endif
+#ifndef QKD_D32_THREADS
+#define QKD_D32_THREADS 512
+#endif
+#define QKD_D32_TG(DMAX) ((DMAX) == 32 ? QKD_D32_THREADS : 512)
+
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -1,0 +1,9 @@
+// decode_inst_32g.cu -- explicit instantiations of decode_kernel (decode_kernel.cuh) launched by kernel_of() in
+// qkd_ldpc.cu; the variants are spread over several translation units so nvcc compiles them in parallel.
+#include "decode_kernel.cuh"
+
+namespace qkd {
+
+template __global__ void decode_kernel<32, false, false, false, false>(const DecParams);
+
+}  // namespace qkd

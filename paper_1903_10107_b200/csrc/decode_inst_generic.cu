@@ -1,0 +1,12 @@
+// decode_inst_generic.cu -- explicit instantiations of decode_kernel (decode_kernel.cuh) launched by kernel_of() in
+// qkd_ldpc.cu; the variants are spread over several translation units so nvcc compiles them in parallel.
+#include "decode_kernel.cuh"
+
+namespace qkd {
+
+template __global__ void decode_kernel<0, true, false, false, false>(const DecParams);
+template __global__ void decode_kernel<0, false, false, false, false>(const DecParams);
+template __global__ void decode_kernel<0, true, false, false, true>(const DecParams);
+template __global__ void decode_kernel<0, false, false, false, true>(const DecParams);
+
+}  // namespace qkd

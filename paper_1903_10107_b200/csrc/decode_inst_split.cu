@@ -1,0 +1,10 @@
+// decode_inst_split.cu -- explicit instantiations of decode_kernel (decode_kernel.cuh) launched by kernel_of() in
+// qkd_ldpc.cu; the variants are spread over several translation units so nvcc compiles them in parallel.
+#include "decode_kernel.cuh"
+
+namespace qkd {
+
+template __global__ void decode_kernel<20, true, true, true, false>(const DecParams);
+template __global__ void decode_kernel<20, true, false, true, false>(const DecParams);
+
+}  // namespace qkd
