@@ -160,6 +160,25 @@ def test_reconcile_host_matches_device_path(gpu):
     assert np.array_equal(succ, o["success"])
 
 
+def test_reconcile_host_pipelined_chunks(gpu):
+    """qkd_reconcile_host on enough frames to run in several pipelined chunks (two internal copy
+    streams chained by events): identical to the device-resident path (syndrome + LLR + decode), which
+    the tests above pin to the oracle; unpinned host memory on purpose (numpy arrays)."""
+    import torch
+
+    w = synth.workload("C5b")
+    F = 90001                                           # > 2 chunks of >= 16 waves; ragged last chunk
+    x, y, _ = w.gen(0, F)
+    code = gpu.QCCode(w.shifts(), w.Z)
+    xs, ys = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    syn = code.syndrome(xs)
+    r = code.decode(code.build_llr(w.qber, ys), syn, w.max_iter, True)
+    bits, iters, succ = code.reconcile_host(w.qber, y, syn.cpu().numpy(), w.max_iter, True)
+    assert np.array_equal(bits, r["bits"].cpu().numpy())
+    assert np.array_equal(iters, r["iters"].cpu().numpy())
+    assert np.array_equal(succ, r["success"].cpu().numpy())
+
+
 @pytest.mark.parametrize("name", ["C5b", "C5a"])
 def test_full_size_sampled(gpu, name):
     """BASELINE configs[4] at full size (65536 frames) in the bench's launch configuration;
