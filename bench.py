@@ -118,6 +118,9 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return None
+        t0 = time.time()   # a timed region shorter than nvidia-smi's start-up: take the first sample after it
+        while not self.rows and time.time() - t0 < 3.0 and self.proc.poll() is None:
+            time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
