@@ -64,7 +64,7 @@ def build_cuda(force: bool = False, extra: list[str] | None = None, out: str | N
     cu = [s for s in srcs if s.endswith(".cu")]
     objdir = os.path.join(os.path.dirname(out), "build_obj")
     os.makedirs(objdir, exist_ok=True)
-    common = [NVCC, *(extra or []), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+    common = [NVCC, *(extra or []), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xfatbin", "-compress-all",
               "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
     jobs = []
     for src in cu:
