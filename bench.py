@@ -33,6 +33,12 @@ import synth  # noqa: E402
 
 METRIC = "corrected-key Mbps at QBER 1-8% (1/2/4/8 GPU); % of HBM roofline per iteration"
 UNIT = "Mbps"
+# The paper's own CPU figures (Table 2): context only -- its codes, frame length and
+# workload are unpublished, so no ratio is formed (vs_baseline stays null).
+PAPER_CONTEXT = {"value": 57.60, "unit": "Mbps", "hardware": "Intel i7-6700HQ, 4 cores (P:54, P:211)",
+                 "also": "122.17 Mbps on an Intel i9-9900K (P:209)", "efficiency": 1.108,
+                 "note": "paper's unpublished ~100 kb codes, bi-directional protocol; not this workload"}
+
 WORKLOADS = {"C5": ["C5a", "C5b"], "C1": ["C1"], "C2": ["C2"], "C3": ["C3"],
              "C4": [f"C4@{q:g}" for q in synth.C4_QBERS]}
 
@@ -394,6 +400,7 @@ def run_gpu(args):
                              "algorithmic_bytes_per_launch": per_wl[dom]["alg_bytes"],
                              "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 4 * len(W) * args.steps,
+                "paper_context": PAPER_CONTEXT,
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:
