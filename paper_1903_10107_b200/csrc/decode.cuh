@@ -51,6 +51,9 @@ constexpr int kFramesPerGroup = 4;   // frames per SWAR word (one byte lane each
 #define QKD_D32_THREADS 512
 #endif
 #define QKD_D32_TG(DMAX) ((DMAX) == 32 ? QKD_D32_THREADS : 512)
+#ifndef QKD_G32_THREADS
+#define QKD_G32_THREADS 256   // variant 8 (degree <= 32, E in global memory): 254 registers, no spills
+#endif
 
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -405,7 +405,7 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
     pl.pow2 = (pl.variant <= 2 || pl.variant == 5 || pl.variant == 6) && ((c->Z & (c->Z - 1)) == 0);   // smem E only
     int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024
-                 : (pl.variant == 2 || pl.variant == 7 ? 512 : (pl.variant >= 6 ? QKD_D32_THREADS : 256));
+                 : (pl.variant == 2 || pl.variant == 7 ? 512 : (pl.variant == 8 ? QKD_G32_THREADS : (pl.variant == 6 ? QKD_D32_THREADS : 256)));
     if (const char* e = std::getenv("QKD_TG_MAX"))   // experiments: fewer threads per frame group
         tg_max = std::max(32, std::min(tg_max, atoi(e) / 32 * 32));
     if (pl.variant == 5)   // two lanes per row, 16 rows per warp
