@@ -181,7 +181,7 @@ int qkd_reconcile_adaptive(const qkd_code* code, double qber, int64_t n_frames,
  *   schedule 0 = layered (the paper's); 1 = flooding: every iteration all
  *   check nodes from the previous state, then E_j = LLR_j + sum_i L_ij (float atomics, so the
  *   summation order -- and the last bits of E -- vary from run to run).
- * Errors: QKD_EINVAL, QKD_EDIM (workspace too small), QKD_EUNSUP (degree > 20), QKD_ECUDA. */
+ * Errors: QKD_EINVAL, QKD_EDIM (workspace too small), QKD_EUNSUP (check degree > 32), QKD_ECUDA. */
 int qkd_build_llr_float(const qkd_code* code, double qber, int64_t n_frames, const uint8_t* bob_bits_dev,
                         const uint8_t* known_bits_dev, float* llr_dev, void* stream);
 size_t qkd_float_workspace_bytes(const qkd_code* code, int64_t n_frames);

@@ -416,3 +416,27 @@ def test_c4_rate_adaptive_recipe_hits_target_efficiency():
         d, p, s = w.rate_adaptive_counts()
         assert d == 36965 and p + s == d
         assert abs(oracle.efficiency(w.m, w.n, p, s, q) - 1.1) < 1e-3
+
+
+def test_check_node_forward_backward_schedule_golden():
+    """R6 pinned on degree 4-6 rows (tests/golden/check_node_fb.json): hand traces of the
+    forward/backward schedule with Algorithm 1.  Each case also records Eq.(7)'s
+    literal per-edge right fold and the per-edge left fold, and differs from both, so an
+    oracle that used either (or any other fold order) fails here even though every degree-3 pin
+    is schedule-free."""
+    g = json.load(open(os.path.join(GOLD, "check_node_fb.json")))
+    assert len(g["cases"]) >= 6
+    for c in g["cases"]:
+        m, fb = c["mag"], c["fb"]
+        assert fb != c["right_fold"] and fb != c["left_fold"]
+        assert [abs(v) for v in oracle.check_node(m, 0)] == fb
+        # the same magnitudes behind x = E - L of either sign and |x| above MSG_max on one edge:
+        # magnitudes are min(|x|, 63) (R3) and the sign rule is Eq.(1) with s_i (R5)
+        x = [(-v if k % 2 else v) for k, v in enumerate(m)]
+        x = [(v + 64 if v == 63 else v) for v in x]
+        out = oracle.check_node(x, 1)
+        for k, v in enumerate(out):
+            assert abs(v) == fb[k]
+            want_neg = (1 + sum(1 for j in range(len(x)) if j != k and x[j] < 0)) % 2
+            if v:
+                assert int(v < 0) == want_neg
