@@ -8,8 +8,8 @@
 // [-190, 190]) is a sum of non-negative 16-bit lanes, and the check node's output byte
 // T = 192 + L_new is stored as computed.
 //
-// Workspace layout: per slot, per block row I, row r owns Dp = roundup4(deg_I) consecutive
-// words (edge k of the row at word k), so a row's messages move with 128-bit loads/stores.
+// Workspace layout: per slot, per block row I, the rows' message words in emission order in up to
+// three dense regions (msg_word below); the lane-pair variant keeps its own row layout.
 #pragma once
 #include "swar.cuh"
 
@@ -17,13 +17,13 @@
 namespace qkd {
 
 struct DecParams {
-    const int4* layer;        // [Mb] (degree, first base edge, L offset in words, Dp)
+    const int4* layer;        // [Mb] (degree, first base edge, L offset in words, words per row)
     const int2* edge;         // [nbase] (J*Z, shift)
     const int* soff;          // [Mb] split-table offset of block row I (entries; split layout only)
     int nsplit;               // split-table entries per slot (sum over I of 2 * HB_I)
     int Mb, Z, nbase, n, m, mb8, nb8;
     long long n_edges;        // canonical message count (nbase * Z)
-    long long ws_words;       // workspace words per slot (sum over I of Z * Dp_I)
+    long long ws_words;       // workspace words per slot (sum over I of Z * words per row)
     const int8_t* llr;        // [F][n]
     const uint8_t* syn;       // [F][mb8]
     long long F, ngroups;
@@ -99,7 +99,7 @@ __device__ __forceinline__ EdgeIn edge_in(uint32_t e, uint32_t tw, const Konst& 
     r.xlo = imad(r.xhi, K.m256, e - tw + 0x01010100u);    // lanes {0,2}: (e + S) - 256 * xhi
     const uint32_t clo = relu_min(r.xlo, K.b128, 0x007E007Eu);   // clamp(X - 128, 0, 126)
     const uint32_t chi = relu_min(r.xhi, K.b128, 0x007E007Eu);
-    r.cw = pack16(clo, chi);          // bytes in [0, 126]; bit 6 = (x >= 1) -- x = 0 counts as
+    r.cw = pack16c(clo, chi, K);      // bytes in [0, 126]; bit 6 = (x >= 1) -- x = 0 counts as
     return r;                         // negative, which is immaterial (R23)
 }
 // check-node magnitude min(|x|, 63) (MSG_max = 63)
@@ -128,7 +128,7 @@ __device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t negf, uint3
     const uint32_t d = sn - t_old + 0x80808080u;                  // IADD3, exact per byte
     const uint32_t hi = imad(hi16z(ew), K.one, hi16z(d));         // lanes {1,3}: ew + d
     const uint32_t lo = imad(hi, K.m256, imad(ew, K.one, d));     // lanes {0,2}
-    const uint32_t enew = pack16(relu_min(lo, K.b128, 0x00FE00FEu), relu_min(hi, K.b128, 0x00FE00FEu));
+    const uint32_t enew = pack16c(relu_min(lo, K.b128, 0x00FE00FEu), relu_min(hi, K.b128, 0x00FE00FEu), K);
     const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);
     return sn;
@@ -145,7 +145,7 @@ __device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t negf, const Ed
     const uint32_t thi = hi16s(Tb);                               // lanes {1,3}: 64 + L_new - 128
     const uint32_t tlo = imad(imad(thi, K.m256, Tb), K.one, 0xFFFFFF00u);   // lanes {0,2}, same
     // E + L_new - L_old = x + L_new: lanes relu(min(X + T - 128, 254)) = clamp(.., -127, 127) + 127
-    const uint32_t enew = pack16(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu));
+    const uint32_t enew = pack16c(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu), K);
     const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);                              // G ? ew : enew
     return Tb;                                                    // 192 + L_new (stored as is)
@@ -160,25 +160,95 @@ __device__ __forceinline__ uint32_t edge_out_c(uint32_t oc, uint32_t negf, const
     const uint32_t Tb = imad(om, K.m2, imad(oc, K.m1, 0xFFFFFFFFu));   // 255 - oc - 2 om = 192 + L_new
     const uint32_t thi = hi16s(Tb);                               // lanes {1,3}: L_new - 64
     const uint32_t tlo = lo16s(Tb);                               // lanes {0,2}: L_new - 64
-    const uint32_t enew = pack16(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu));
+    const uint32_t enew = pack16c(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu), K);
     const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);
     return Tb;                                                    // 192 + L_new
 }
 
 __device__ __forceinline__ uint4 ld4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+// global 128-bit store / load kept in program order with the other volatile accesses of the row
+// (the table reloads): ptxas otherwise sinks a row's message stores to its end, and with them the
+// next row's prefetch loads, which may alias them as far as it knows
+__device__ __forceinline__ void st4_pinned(uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void ld4_pinned(const uint32_t* p, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+    asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p) : "memory");
+}
 __device__ __forceinline__ void st4(uint32_t* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
 __device__ __forceinline__ uint32_t& w4(uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
+// ---- message layout (every variant but the lane-pair one) -----------------------------------
+// Row r of a block row of degree D keeps its D message words in EMISSION order (word p = the
+// p-th edge row_update emits, emit_pos below), spread over up to three dense regions of the
+// block row's workspace (li.z words from the slot base): main (D/4 uint4 per row, group-major:
+// group g of row r at word (g Z + r) 4, so a warp's group access is one contiguous 512-byte
+// block), tail2 (one uint2 per row when D % 4 >= 2) and tail1 (one word per row when D is odd).
+// Every access is aligned and coalesced, rows are stored as soon as their words are final, and
+// no padding word is ever loaded or stored (the write traffic equals the algorithmic bytes).
+__host__ __device__ constexpr int emit_pos(int D, int k) {    // emission step of edge k
+    return k >= D / 2 ? 2 * (k - D / 2) : 2 * (D / 2 - 1 - k) + 1;
+}
+__host__ __device__ constexpr int emit_edge(int D, int p) {   // edge emitted at step p
+    return (p & 1) ? D / 2 - 1 - (p >> 1) : D / 2 + (p >> 1);
+}
+// address of word p of row r (block row of degree D at word offset base)
+__device__ __forceinline__ uint32_t* msg_word(uint32_t* Lslot, int base, int D, int Z, int r, int p) {
+    const int q4 = D & ~3;
+    uint32_t* b = Lslot + base;
+    if (p < q4) return b + (long long)(p >> 2) * 4 * Z + 4 * r + (p & 3);
+    if (p < q4 + (D & 2)) return b + (long long)Z * q4 + 2 * r + (p - q4);
+    return b + (long long)Z * (q4 + (D & 2)) + r;
+}
+// the thread's next row (message prefetch target): degree D (0 = none), block-row base, row
+struct NextRow {
+    int base, D, r;
+};
+
+// Registers of a row's message words: word q < 4*(D/4) in S[q], the tail2 words in S[SW-4],
+// S[SW-3] and the tail1 word in S[SW-1] (fixed slots, so a row of run-time degree -- the next
+// row, prefetched -- loads without dynamic register indexing; main words never reach them, as
+// 4*(D/4) <= SW - 4 whenever D has a tail).
+template <int SW>
+__host__ __device__ constexpr int msg_slot(int D, int q) {
+    return q < (D & ~3) ? q : (q < (D & ~3) + (D & 2) ? SW - 4 + (q - (D & ~3)) : SW - 1);
+}
+// load the words of row r (block row of degree D) into S, main groups from `from_group` on
+template <int SW>
+__device__ __forceinline__ void msg_load(uint32_t* Lslot, int base, int D, int Z, int r, uint32_t (&S)[SW], int from_group) {
+    const int q4 = D & ~3;
+    const uint32_t* m = Lslot + base + 4 * r;
+#pragma unroll
+    for (int g = 0; g < SW / 4; ++g)
+        if (g >= from_group && 4 * g < q4) {
+            const uint4 v = ld4(m + (long long)g * 4 * Z);
+            S[4 * g] = v.x; S[4 * g + 1] = v.y; S[4 * g + 2] = v.z; S[4 * g + 3] = v.w;
+        }
+    if (D & 2) {
+        const uint2 v = *reinterpret_cast<const uint2*>(Lslot + base + (long long)Z * q4 + 2 * r);
+        S[SW - 4] = v.x;
+        S[SW - 3] = v.y;
+    }
+    if (D & 1) S[SW - 1] = Lslot[base + (long long)Z * (q4 + (D & 2)) + r];
+}
+
 // One check row r of a block row with D edges (layered update, Alg. 1/2).
-//   et   : the row's D (cb, s) entries;  Lrow : this row's Dp words;  nib : target syndrome bits
+//   et   : the row's D (cb, s) entries;  S : the row's message words (emission order), loaded here
+//          unless `have` (prefetched by the previous row) or `first`;  nib : target syndrome bits
 //   first: all four lanes start a frame with this sweep -- messages are L = 0 (R16), not loaded.
 //   (A lane refilled alone has its bytes of the workspace reset to T = 192 when its frame is loaded.)
-template <int D, bool ESM, bool POW2, int KEEP_ADDR_MAX = 10>
+//   PF   : while emitting, load the next row's (nx) message words into S as this row's words are
+//          stored, so the next row's global-memory latency overlaps this row's arithmetic.
+//   FM   : 0 = `first` read at run time, 1 = first sweep (compile time), 2 = not the first sweep.
+template <int D, bool ESM, bool POW2, int KEEP_ADDR_MAX, bool PF, int FM, int SW>
 __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, uint32_t r4, uint32_t zm4,
-                                           unsigned char* Eb, uint32_t* __restrict__ Lrow, uint32_t nib,
-                                           bool first, const Konst& K) {
-    constexpr int NV = (D + 3) / 4;
+                                           unsigned char* Eb, uint32_t* __restrict__ Lslot, int base, int r,
+                                           uint32_t (&S)[SW], bool have, const NextRow nx, uint32_t nib,
+                                           bool first_rt, const Konst& K) {
+    const bool first = FM == 1 || (FM == 0 && first_rt);
+    static_assert(SW % 4 == 0 && SW >= ((D + 3) & ~3) && (D % 4 == 0 || (D & ~3) <= SW - 4), "message register array");
+    constexpr int Q4 = D & ~3;
     // High degrees recompute each E address in the emit phase (one smem table load + IMAD + LOP3)
     // instead of holding D addresses in registers through the forward/backward passes.
     constexpr bool KEEP_ADDR = D <= KEEP_ADDR_MAX;
@@ -189,38 +259,40 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
 #define QKD_LOWREG_MIN 21
 #endif
     constexpr bool LOWREG = D >= QKD_LOWREG_MIN;
-    uint4 S[NV];
     uint32_t addr[D];
     EdgeIn in[D];
     uint32_t P = 0;
+    if (first) {
 #pragma unroll
-    for (int v = 0; v < NV; ++v) S[v] = first ? make_uint4(0xC0C0C0C0u, 0xC0C0C0C0u, 0xC0C0C0C0u, 0xC0C0C0C0u)
-                                              : ld4(Lrow + 4 * v);
+        for (int q = 0; q < SW; ++q) S[q] = 0xC0C0C0C0u;
+    } else if (!have) {
+        msg_load(Lslot, base, D, Z, r, S, 0);
+    }
 #pragma unroll
     for (int k = 0; k < D; ++k) addr[k] = Addr<POW2>::at(et[k], r4, zm4, Z, K);
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-        in[k] = edge_in(ldE<ESM>(Eb, addr[k]), w4(S[k >> 2], k & 3), K);
+    for (int q = 0; q < D; ++q) {      // gather in emission order: the last-prefetched words last
+        const int k = emit_edge(D, q);
+        in[k] = edge_in(ldE<ESM>(Eb, addr[k]), S[msg_slot<SW>(D, q)], K);
         P ^= in[k].cw;
     }
     // Eq.(1) with the target bit: L_new of edge k is negative iff
     // s_i ^ XOR_{j != k} [x_j < 0] = s_i ^ ((D-1)&1) ^ P ^ nonneg_k   (bit 6)
     const uint32_t Q = P ^ nib_to_bit6(nib) ^ (((D - 1) & 1) ? 0x40404040u : 0u);
-    // emit edge k as soon as its leave-one-out magnitude is known (keeps the live set small)
-    // Leave-one-out by the forward/backward schedule of R6, evaluated meet-in-the-middle: the
-    // forward chain over edges [0, H) and the backward chain over [H, D) run concurrently, then
-    // each continues across the other half while emitting outputs.  Every tau has exactly the
-    // arguments of the plain F/B schedule (F_k = tau(F_{k-1}, m_k), B_k = tau(m_k, B_{k+1}),
-    // o_k = tau(F_{k-1}, B_{k+1})), so results are identical; two independent chains double the ILP.
-    constexpr int H = D / 2;
-    auto step_of = [](int k) { return k >= H ? 2 * (k - H) : 2 * (H - 1 - k) + 1; };   // emission order
-    auto last_of_group = [&](int k) {   // is k the last-emitted edge of its 128-bit group?
-        int best = -1, arg = -1;
-        for (int q = k & ~3; q < (k & ~3) + 4 && q < D; ++q)
-            if (step_of(q) > best) { best = step_of(q); arg = q; }
-        return arg == k;
-    };
+    // group g of this row at Lm + g 4Z, of the next row at Ln + g 4Z.  The pointers are opaque
+    // GENERIC pointers: ptxas keeps generic accesses in order with the row's shared-memory E
+    // accesses (they might alias), which pins each group store, and the next row's load into
+    // the registers it frees, where the source puts them -- with global pointers it sinks all of
+    // them to the end of the row and the prefetch hides nothing.
+    uint32_t *Lm, *Ln;
+    asm("mov.b64 %0, %1;" : "=l"(Lm) : "l"(Lslot + base + 4 * r));
+    if constexpr (PF) asm("mov.b64 %0, %1;" : "=l"(Ln) : "l"(Lslot + nx.base + 4 * nx.r));
+    const long long zs = 4LL * Z;
+    // emit edge k as soon as its leave-one-out magnitude is known (keeps the live set small); its
+    // message word sits at position q = emit_pos(D, k), and positions are emitted in increasing
+    // order, so a uint4 group is final (stored, then refilled with the next row's words) at q % 4 == 3
     auto emit = [&](int k, uint32_t o) {
+        const int q = emit_pos(D, k), sl = msg_slot<SW>(D, q);
         uint32_t a;
         if constexpr (KEEP_ADDR) {
             a = addr[k];
@@ -232,11 +304,23 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         const uint32_t ew = ldE<ESM>(Eb, a);
         uint32_t eo;
         if constexpr (LOWREG)
-            w4(S[k >> 2], k & 3) = edge_out_s(o, Q ^ in[k].cw, w4(S[k >> 2], k & 3), ew, K, eo);
+            S[sl] = edge_out_s(o, Q ^ in[k].cw, S[sl], ew, K, eo);
         else
-            w4(S[k >> 2], k & 3) = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
+            S[sl] = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
         stE<ESM>(Eb, a, eo);
-        if (D <= 2 ? (k == 0) : last_of_group(k)) st4(Lrow + (k & ~3), S[k >> 2]);
+        if (q < Q4 && (q & 3) == 3) {
+            const int g = q >> 2;
+            st4(Lm + g * zs, make_uint4(S[4 * g], S[4 * g + 1], S[4 * g + 2], S[4 * g + 3]));
+            if constexpr (PF) {   // the next row's group g into the registers just stored
+                if (4 * g < (nx.D & ~3)) {
+                    const uint4 v = ld4(Ln + g * zs);
+                    S[4 * g] = v.x; S[4 * g + 1] = v.y; S[4 * g + 2] = v.z; S[4 * g + 3] = v.w;
+                }
+            }
+        } else if ((D & 2) && q == Q4 + 1) {
+            *reinterpret_cast<uint2*>(Lslot + base + (long long)Z * Q4 + 2 * r) = make_uint2(S[SW - 4], S[SW - 3]);
+        }
+        if ((D & 1) && q == D - 1) Lslot[base + (long long)Z * (Q4 + (D & 2)) + r] = S[SW - 1];
     };
     // magnitudes in complement form (tau4c / edge_magc / edge_out_c): two instructions fewer per tau
 #define QKD_TAU tau4c
@@ -248,6 +332,12 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         emit(1, QKD_MAG(in[0].cw, K));
         emit(0, QKD_MAG(in[1].cw, K));
     } else {
+        // Leave-one-out by the forward/backward schedule of R6, evaluated meet-in-the-middle: the
+        // forward chain over edges [0, H) and the backward chain over [H, D) run concurrently, then
+        // each continues across the other half while emitting outputs.  Every tau has exactly the
+        // arguments of the plain F/B schedule (F_k = tau(F_{k-1}, m_k), B_k = tau(m_k, B_{k+1}),
+        // o_k = tau(F_{k-1}, B_{k+1})), so results are identical; two independent chains double the ILP.
+        constexpr int H = D / 2;
         uint32_t F[H], B[D];                        // F_0..F_{H-1}; B_H..B_{D-1}
         F[0] = QKD_MAG(in[0].cw, K);
         B[D - 1] = QKD_MAG(in[D - 1].cw, K);
@@ -259,7 +349,7 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         }
         uint32_t f = F[H - 1], b = B[H];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {               // phase 2: continue across, emitting
+        for (int j = 0; j < D; ++j) {               // phase 2: continue across, emitting (steps 2j, 2j+1)
             const int kf = H + j;                   // forward: o_kf = tau(F_{kf-1}, B_{kf+1})
             if (kf <= D - 2) {
                 emit(kf, QKD_TAU(f, B[kf + 1], K));
@@ -279,6 +369,9 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
 #undef QKD_TAU
 #undef QKD_MAG
 #undef QKD_O63
+    if constexpr (PF) {   // the next row's groups beyond this row's and its tail words
+        if (nx.D > 0) msg_load(Lslot, nx.base, nx.D, Z, nx.r, S, Q4 / 4);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -377,14 +470,16 @@ __device__ __forceinline__ uint32_t syndrome_row(const int2* __restrict__ et, in
 // Runtime-degree variant (any degree <= 64), same arithmetic; state in local memory.
 template <bool ESM>
 __device__ __noinline__ void row_update_generic(const int2* __restrict__ et, int D, int Z, uint32_t r4,
-                                                unsigned char* Eb, uint32_t* __restrict__ Lrow, uint32_t nib,
-                                                bool first, const Konst K) {
+                                                unsigned char* Eb, uint32_t* __restrict__ Lslot, int base, int r,
+                                                uint32_t nib, bool first, const Konst K) {
     uint32_t addr[64], S[64], F[64], o[64];
+    uint32_t* wp[64];
     EdgeIn in[64];
     uint32_t P = 0;
     for (int k = 0; k < D; ++k) {
         addr[k] = Addr<false>::at(et[k], r4, 0u, Z, K);
-        S[k] = first ? 0xC0C0C0C0u : Lrow[k];
+        wp[k] = msg_word(Lslot, base, D, Z, r, emit_pos(D, k));   // same layout as row_update
+        S[k] = first ? 0xC0C0C0C0u : *wp[k];
         in[k] = edge_in(ldE<ESM>(Eb, addr[k]), S[k], K);
         P ^= in[k].cw;
     }
@@ -408,7 +503,7 @@ __device__ __noinline__ void row_update_generic(const int2* __restrict__ et, int
     for (int k = 0; k < D; ++k) {
         const uint32_t ew = ldE<ESM>(Eb, addr[k]);
         uint32_t eo;
-        Lrow[k] = edge_out(o[k], Q ^ in[k].cw, in[k], ew, K, eo);
+        *wp[k] = edge_out(o[k], Q ^ in[k].cw, in[k], ew, K, eo);
         stE<ESM>(Eb, addr[k], eo);
     }
 }

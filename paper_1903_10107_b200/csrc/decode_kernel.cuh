@@ -13,10 +13,28 @@
 namespace qkd {
 
 
-template <int DMAX, bool ESM, bool POW2, bool SPLIT>
-__device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, const int2* et, int t,
+#ifndef QKD_PF_DMAX
+#define QKD_PF_DMAX 0   // decode variant (DMAX) that prefetches the next row's messages (0: none, -1: all; measured slower on C5a: +6% SASS)
+#endif
+template <int DMAX, bool SPLIT>
+struct Prefetch {
+    static constexpr bool on = !SPLIT && DMAX > 0 && (DMAX == QKD_PF_DMAX || QKD_PF_DMAX < 0);
+};
+
+// registers for one row's message words (decode.cuh msg_slot)
+template <int DMAX>
+struct MsgRegs {
+    static constexpr int SW = DMAX > 0 ? ((DMAX + 3) & ~3) : 4;
+};
+
+// One layer (block row) of the slot's rows.  S/have: message words of this thread's next row,
+// prefetched by the previous row when PF (kept across block rows and the block-row barrier:
+// a row's messages are only ever written by the thread that owns the row).  lin = the next
+// block row's layer entry (prefetch target after this block row's last row).
+template <int DMAX, bool ESM, bool POW2, bool SPLIT, bool PF, int FM = 0>
+__device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, const int4 lin, const int2* et, int t,
                                            unsigned char* Eb, uint32_t* Lslot, const uint8_t* synI, uint32_t fresh,
-                                           const Konst& K) {
+                                           uint32_t (&S)[MsgRegs<DMAX>::SW], bool& have, const Konst& K) {
     const bool first = fresh == 0xFu;   // all four lanes on their first sweep: L = 0 without loading
     const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
     if (li.x == 0) return;              // a check row with no variables: nothing to update (oracle: no-op)
@@ -48,8 +66,13 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
 #define QKD_CASE(DD)                                                                                     \
     case DD:                                                                                             \
         if constexpr (DD <= DMAX) {                                                                      \
-            for (int r = t; r < p.Z; r += p.TG)                                                          \
-                row_update<DD, ESM, POW2, (DMAX <= 8 ? 4 : QKD_KEEP_ADDR)>(et, p.Z, 4u * r, zm4, Eb, Lslot + li.z + r * li.w, synI[r], first, K); \
+            for (int r = t; r < p.Z; r += p.TG) {                                                        \
+                const bool more = r + p.TG < p.Z;                                                        \
+                const NextRow nx{more ? li.z : lin.z, PF ? (more ? DD : lin.x) : 0, more ? r + p.TG : t}; \
+                row_update<DD, ESM, POW2, (DMAX <= 8 ? 4 : QKD_KEEP_ADDR), PF, FM>(et, p.Z, 4u * r, zm4, Eb, Lslot, li.z, r, \
+                                                                               S, have, nx, synI[r], first, K); \
+                have = PF && nx.D > 0;                                                                   \
+            }                                                                                            \
             return;                                                                                      \
         }                                                                                                \
         break;
@@ -65,7 +88,7 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
         __trap();   // the host never selects a DMAX kernel for a code with a larger degree
     } else {
         for (int r = t; r < p.Z; r += p.TG)
-            row_update_generic<ESM>(et, li.x, p.Z, 4u * r, Eb, Lslot + li.z + r * li.w, synI[r], first, K);
+            row_update_generic<ESM>(et, li.x, p.Z, 4u * r, Eb, Lslot, li.z, r, synI[r], first, K);
     }
 }
 
@@ -155,13 +178,14 @@ static __device__ void finalize(const DecParams& p, const int4* s_layer, const u
                 for (int q = t; q < cnt; q += p.TG) {
                     const int k = q / p.Z, r = q - k * p.Z;
                     const long long e = (long long)(li.y + k) * p.Z + r;     // canonical edge order
-                    int wk = k;   // word of canonical edge k inside the row (split: side A, then side B)
+                    const uint32_t* wp;   // word of canonical edge k (split: side A, then side B)
                     if (p.soff) {
                         const int ha = li.x >> 1;
-                        wk = k < ha ? k : ((ha + 1) & ~1) + (li.x - 1 - k);
+                        wp = Lslot + li.z + r * li.w + (k < ha ? k : ((ha + 1) & ~1) + (li.x - 1 - k));
+                    } else {
+                        wp = msg_word(const_cast<uint32_t*>(Lslot), li.z, li.x, p.Z, r, emit_pos(li.x, k));
                     }
-                    lrow[e] = first ? (int8_t)0
-                                    : (int8_t)((int)((Lslot[li.z + r * li.w + wk] >> (8 * f)) & 0xFFu) - 192);
+                    lrow[e] = first ? (int8_t)0 : (int8_t)((int)((*wp >> (8 * f)) & 0xFFu) - 192);
                 }
             }
         }
@@ -224,6 +248,8 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
     int* ctl = reinterpret_cast<int*>(sSyn + ((p.m + 15) & ~15));   // [0] group id, [1..2] flags
     uint32_t* flags = reinterpret_cast<uint32_t*>(ctl + 1);
     uint32_t* Lslot = p.Lws + gslot * p.ws_words;
+    uint32_t S[MsgRegs<DMAX>::SW];   // this thread's next row's message words (prefetched when Prefetch::on)
+    bool have = false;
 
     if constexpr (!SPLIT && REFILL) {
         // ---- per-frame scheduling: a lane whose frame stops is refilled with the next frame at
@@ -353,8 +379,8 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
             if (!active) break;
             for (int I = 0; I < p.Mb; ++I) {   // idle lanes (no frame left) compute harmlessly
                 const int4 li = s_layer[I];
-                layer_pass<DMAX, ESM, POW2, SPLIT>(p, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,
-                                                   fresh == 0xFu ? 0xFu : 0u, K);
+                layer_pass<DMAX, ESM, POW2, SPLIT, false>(p, li, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,
+                                                          fresh == 0xFu ? 0xFu : 0u, S, have, K);
                 group_bar(bar, p.TG);
             }
             ++sweeps;
@@ -444,15 +470,25 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
             active &= viol;
         }
         int it = 0;
+        // one sweep over the block rows; the first sweep of a group (L = 0, R16) is a separate
+        // instance so the row update carries no run-time `first` test
+#define QKD_SWEEP(FM)                                                                                    \
+    for (int I = 0; I < p.Mb; ++I) {                                                                     \
+        const int4 li = s_layer[I];                                                                      \
+        const int4 lin = s_layer[I + 1 < p.Mb ? I + 1 : 0];                                              \
+        layer_pass<DMAX, ESM, POW2, SPLIT, Prefetch<DMAX, SPLIT>::on, FM>(                               \
+            p, li, lin, SPLIT ? s_edge2 + s_soff[I] : s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,       \
+            FM == 1 ? 0xFu : 0u, S, have, K);                                                            \
+        group_bar(bar, p.TG);                                                                            \
+    }
         while (active && it < p.T) {
             ++it;
-            const uint32_t fresh = it == 1 ? 0xFu : 0u;
-            for (int I = 0; I < p.Mb; ++I) {
-                const int4 li = s_layer[I];
-                layer_pass<DMAX, ESM, POW2, SPLIT>(p, li, SPLIT ? s_edge2 + s_soff[I] : s_edge + li.y, t, Eb, Lslot,
-                                                   sSyn + I * p.Z, fresh, K);
-                group_bar(bar, p.TG);
+            if (it == 1) {
+                QKD_SWEEP(1)
+            } else {
+                QKD_SWEEP(2)
             }
+#undef QKD_SWEEP
             if (p.early_stop) {
                 const uint32_t viol = syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
                 const uint32_t done = active & ~viol;

@@ -43,7 +43,7 @@ struct qkd_code {
     int64_t n = 0, m = 0, n_edges = 0;
     int32_t nbase = 0, maxdeg = 0;
     std::vector<int4> layer;   // (deg, first base edge, workspace word offset of the block row, Dp)
-    int64_t ws_words = 0;      // workspace words per slot: sum_I Z * roundup4(deg_I)
+    int64_t ws_words = 0;      // workspace words per slot: sum_I Z * deg_I (lane-pair layout: padded rows)
     std::vector<int2> edge;    // (J*Z, shift)
     int4* d_layer = nullptr;
     int2* d_edge = nullptr;
@@ -372,7 +372,7 @@ const void* kernel_of(int variant, bool pow2, bool refill = false) {
 
 // 1, 2, -1, -2, -256 as kernel arguments: opaque to ptxas, so a*one + c stays an IMAD (FMA pipe)
 Konst runtime_konst() {
-    return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu};
+    return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu, 0u, 256u};
 }
 
 // Decode variant of a code on a device (fixed at code creation: the split variant has its own
@@ -511,11 +511,12 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
             li.w = ((ha + 1) & ~1) + ((hb + 1) & ~1);
             c->soff.push_back(c->nsplit);
             c->nsplit += 2 * hb;
-        } else {
-            li.w = (li.x + 3) & ~3;
+        } else {   // D words per row in emission order, dense regions (decode.cuh msg_word)
+            li.w = li.x;
         }
         li.z = (int)c->ws_words;
         c->ws_words += (int64_t)Z * li.w;
+        c->ws_words = (c->ws_words + 3) & ~3LL;   // every block row's regions start 16-byte aligned
         if (c->ws_words > (1LL << 31) - 1) {
             delete c;
             return fail(QKD_EUNSUP, "code too large for the 32-bit workspace offsets");

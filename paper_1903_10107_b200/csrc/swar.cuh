@@ -13,12 +13,12 @@
 
 namespace qkd {
 
-// runtime constants 1, 2, -1, -2, -256, the lane bias -128|-128 and the byte constants
-// 0x3F3F3F3F / 0x7F7F7F7F (kernel parameters, opaque
+// runtime constants 1, 2, -1, -2, -256, the lane bias -128|-128, the byte constants
+// 0x3F3F3F3F / 0x7F7F7F7F, 0 and 256 (kernel parameters, opaque
 // to the compiler); in_regs() pins them in ordinary registers so ptxas neither folds them nor
 // re-materialises them per use.
 struct Konst {
-    uint32_t one, two, m1, m2, m256, b128, c63, c127;
+    uint32_t one, two, m1, m2, m256, b128, c63, c127, zero, p256;
     __device__ __forceinline__ Konst in_regs() const {
         Konst k;
         asm volatile("mov.b32 %0, %1;" : "=r"(k.one) : "r"(one));
@@ -29,6 +29,8 @@ struct Konst {
         asm volatile("mov.b32 %0, %1;" : "=r"(k.b128) : "r"(b128));
         asm volatile("mov.b32 %0, %1;" : "=r"(k.c63) : "r"(c63));
         asm volatile("mov.b32 %0, %1;" : "=r"(k.c127) : "r"(c127));
+        k.zero = zero;   // used only as an opaque operand (scheduling dependencies), not pinned
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.p256) : "r"(p256));
         return k;
     }
 };
@@ -114,6 +116,8 @@ __device__ __forceinline__ uint32_t hi16z(uint32_t w) { return prmt<0x4341u>(w, 
 __device__ __forceinline__ uint32_t lo16s(uint32_t w) { return prmt<0xA280u>(w, 0u); }
 // pack the low bytes of two 16x2 words back into frame order {0,1,2,3}
 __device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi) { return prmt<0x6240u>(lo, hi); }
+// the same for clean lanes (every 16-bit lane in [0, 255]) on the FMA pipe: lo + 256 hi
+__device__ __forceinline__ uint32_t pack16c(uint32_t lo, uint32_t hi, const Konst& K) { return imad(hi, K.p256, lo); }
 // byte mask 0xFF where bit 7 of the byte is set
 __device__ __forceinline__ uint32_t bmask7(uint32_t w) { return prmt<0xBA98u>(w, 0u); }
 
