@@ -8,8 +8,8 @@
 // [-190, 190]) is a sum of non-negative 16-bit lanes, and the check node's output byte
 // T = 192 + L_new is stored as computed.
 //
-// Workspace layout: per slot, per block row I, the rows' message words in emission order in up to
-// three dense regions (msg_word below); the lane-pair variant keeps its own row layout.
+// Workspace layout: per slot, per block row I, the rows' message words in emission order,
+// position-major (msg_word below); the lane-pair variant keeps its own row layout.
 #pragma once
 #include "swar.cuh"
 
@@ -96,7 +96,7 @@ __device__ __forceinline__ EdgeIn edge_in(uint32_t e, uint32_t tw, const Konst& 
     // lanes {1,3}: e + 256 - T.  prmt(e, one) = hi16z(e) with byte 0 of K.one (0x01) in bytes 1, 3,
     // i.e. + 0x01000100, so the subtraction stays one IMAD (FMA pipe)
     r.xhi = imad(hi16z(tw), K.m1, prmt<0x4341u>(e, K.one));
-    r.xlo = imad(r.xhi, K.m256, e - tw + 0x01010100u);    // lanes {0,2}: (e + S) - 256 * xhi
+    r.xlo = imadi<-256>(r.xhi, e - tw + 0x01010100u);    // lanes {0,2}: (e + S) - 256 * xhi
     const uint32_t clo = relu_min(r.xlo, K.b128, 0x007E007Eu);   // clamp(X - 128, 0, 126)
     const uint32_t chi = relu_min(r.xhi, K.b128, 0x007E007Eu);
     r.cw = pack16c(clo, chi, K);      // bytes in [0, 126]; bit 6 = (x >= 1) -- x = 0 counts as
@@ -122,12 +122,12 @@ __device__ __forceinline__ uint32_t edge_magc_alt(uint32_t cw) { return 0x3F3F3F
 // keeps ew where |E| = 127.  Returns T_new.
 __device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t negf, uint32_t t_old, uint32_t ew,
                                                const Konst& K, uint32_t& e_out) {
-    const uint32_t M = bmask7(imad(negf, K.two, 0u));             // 0xFF where L_new < 0
+    const uint32_t M = bmask7(imadi<2>(negf, 0u));             // 0xFF where L_new < 0
     const uint32_t nx = lop3i<0x87, 0x7F7F7F7Fu>(oc, M);          // ~(oc ^ (M & 0x7F))
     const uint32_t sn = imad(lop3i<0xA0, 0x01010101u>(M, 0u), K.one, nx);   // + (M & 1)
     const uint32_t d = sn - t_old + 0x80808080u;                  // IADD3, exact per byte
     const uint32_t hi = imad(hi16z(ew), K.one, hi16z(d));         // lanes {1,3}: ew + d
-    const uint32_t lo = imad(hi, K.m256, imad(ew, K.one, d));     // lanes {0,2}
+    const uint32_t lo = imadi<-256>(hi, imad(ew, K.one, d));     // lanes {0,2}
     const uint32_t enew = pack16c(relu_min(lo, K.b128, 0x00FE00FEu), relu_min(hi, K.b128, 0x00FE00FEu), K);
     const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);
@@ -139,7 +139,7 @@ __device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t negf, uint3
 // E word (Algorithm 2 guard on |E| = E_max, Eq.(9) saturated to +-127).
 __device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t negf, const EdgeIn& in, uint32_t ew,
                                              const Konst& K, uint32_t& e_out) {
-    const uint32_t M = bmask7(imad(negf, K.two, 0u));             // 0xFF where L_new < 0
+    const uint32_t M = bmask7(imadi<2>(negf, 0u));             // 0xFF where L_new < 0
     const uint32_t om = o & M;
     const uint32_t Tb = imad(om, K.m2, imad(o, K.one, 0xC0C0C0C0u));   // bytes (64 + L_new) + 128
     const uint32_t thi = hi16s(Tb);                               // lanes {1,3}: 64 + L_new - 128
@@ -155,9 +155,9 @@ __device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t negf, const Ed
 // o & M = (oc ^ 63) & M is still one LOP3 and o + 0xC0 = 0xFF - oc one IMAD, so nothing is added.
 __device__ __forceinline__ uint32_t edge_out_c(uint32_t oc, uint32_t negf, const EdgeIn& in, uint32_t ew,
                                                const Konst& K, uint32_t& e_out) {
-    const uint32_t M = bmask7(imad(negf, K.two, 0u));             // 0xFF where L_new < 0
+    const uint32_t M = bmask7(imadi<2>(negf, 0u));             // 0xFF where L_new < 0
     const uint32_t om = lop3i<0x48, 0x3F3F3F3Fu>(oc, M);          // (oc ^ 63) & M = o & M
-    const uint32_t Tb = imad(om, K.m2, imad(oc, K.m1, 0xFFFFFFFFu));   // 255 - oc - 2 om = 192 + L_new
+    const uint32_t Tb = imadi<-2>(om, imad(oc, K.m1, 0xFFFFFFFFu));   // 255 - oc - 2 om = 192 + L_new
     const uint32_t thi = hi16s(Tb);                               // lanes {1,3}: L_new - 64
     const uint32_t tlo = lo16s(Tb);                               // lanes {0,2}: L_new - 64
     const uint32_t enew = pack16c(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu), K);
@@ -180,81 +180,57 @@ __device__ __forceinline__ void st4(uint32_t* p, uint4 v) { *reinterpret_cast<ui
 __device__ __forceinline__ uint32_t& w4(uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
 // ---- message layout (every variant but the lane-pair one) -----------------------------------
-// Row r of a block row of degree D keeps its D message words in EMISSION order (word p = the
-// p-th edge row_update emits, emit_pos below), spread over up to three dense regions of the
-// block row's workspace (li.z words from the slot base): main (D/4 uint4 per row, group-major:
-// group g of row r at word (g Z + r) 4, so a warp's group access is one contiguous 512-byte
-// block), tail2 (one uint2 per row when D % 4 >= 2) and tail1 (one word per row when D is odd).
-// Every access is aligned and coalesced, rows are stored as soon as their words are final, and
-// no padding word is ever loaded or stored (the write traffic equals the algorithmic bytes).
+// Row r of a block row of degree D keeps its D message words in EMISSION order (word q = the
+// q-th edge row_update emits, emit_pos below), interleaved by 32-row chunks: word q of row r at
+// base + (r / 32) 32 D + 32 q + r % 32 (base = li.z words from the slot base).  A warp's access
+// to one position is 128 contiguous bytes, a thread's words are at immediate offsets 128 q from
+// one pointer, no padding word is ever moved (write traffic = the algorithmic bytes), a row's
+// words are stored one by one as they are emitted (nothing buffered in registers for a vector
+// store) and the next row's words can be loaded as soon as this row's gather has consumed its own.
 __host__ __device__ constexpr int emit_pos(int D, int k) {    // emission step of edge k
     return k >= D / 2 ? 2 * (k - D / 2) : 2 * (D / 2 - 1 - k) + 1;
 }
 __host__ __device__ constexpr int emit_edge(int D, int p) {   // edge emitted at step p
     return (p & 1) ? D / 2 - 1 - (p >> 1) : D / 2 + (p >> 1);
 }
-// address of word p of row r (block row of degree D at word offset base)
-__device__ __forceinline__ uint32_t* msg_word(uint32_t* Lslot, int base, int D, int Z, int r, int p) {
-    const int q4 = D & ~3;
-    uint32_t* b = Lslot + base;
-    if (p < q4) return b + (long long)(p >> 2) * 4 * Z + 4 * r + (p & 3);
-    if (p < q4 + (D & 2)) return b + (long long)Z * q4 + 2 * r + (p - q4);
-    return b + (long long)Z * (q4 + (D & 2)) + r;
+// word 0 of row r (block row of degree D at word offset base); word q is at + 32 q
+__device__ __forceinline__ uint32_t* msg_row(uint32_t* Lslot, int base, int D, int r) {
+    return Lslot + base + (r >> 5) * 32 * D + (r & 31);
 }
+__device__ __forceinline__ uint32_t* msg_word(uint32_t* Lslot, int base, int D, int Z, int r, int q) {
+    return msg_row(Lslot, base, D, r) + 32 * q;
+}
+#ifndef QKD_PF_WORDS
+#define QKD_PF_WORDS 32   // prefetch at most this many positions (the rest load at the row's start)
+#endif
 // the thread's next row (message prefetch target): degree D (0 = none), block-row base, row
 struct NextRow {
     int base, D, r;
 };
 
-// Registers of a row's message words: word q < 4*(D/4) in S[q], the tail2 words in S[SW-4],
-// S[SW-3] and the tail1 word in S[SW-1] (fixed slots, so a row of run-time degree -- the next
-// row, prefetched -- loads without dynamic register indexing; main words never reach them, as
-// 4*(D/4) <= SW - 4 whenever D has a tail).
-template <int SW>
-__host__ __device__ constexpr int msg_slot(int D, int q) {
-    return q < (D & ~3) ? q : (q < (D & ~3) + (D & 2) ? SW - 4 + (q - (D & ~3)) : SW - 1);
-}
-// load the words of row r (block row of degree D) into S, main groups from `from_group` on
-template <int SW>
-__device__ __forceinline__ void msg_load(uint32_t* Lslot, int base, int D, int Z, int r, uint32_t (&S)[SW], int from_group) {
-    const int q4 = D & ~3;
-    const uint32_t* m = Lslot + base + 4 * r;
-#pragma unroll
-    for (int g = 0; g < SW / 4; ++g)
-        if (g >= from_group && 4 * g < q4) {
-            const uint4 v = ld4(m + (long long)g * 4 * Z);
-            S[4 * g] = v.x; S[4 * g + 1] = v.y; S[4 * g + 2] = v.z; S[4 * g + 3] = v.w;
-        }
-    if (D & 2) {
-        const uint2 v = *reinterpret_cast<const uint2*>(Lslot + base + (long long)Z * q4 + 2 * r);
-        S[SW - 4] = v.x;
-        S[SW - 3] = v.y;
-    }
-    if (D & 1) S[SW - 1] = Lslot[base + (long long)Z * (q4 + (D & 2)) + r];
-}
-
 // One check row r of a block row with D edges (layered update, Alg. 1/2).
 //   et   : the row's D (cb, s) entries;  S : the row's message words (emission order), loaded here
-//          unless `have` (prefetched by the previous row) or `first`;  nib : target syndrome bits
-//   first: all four lanes start a frame with this sweep -- messages are L = 0 (R16), not loaded.
+//          unless `have` (prefetched by the previous row) or the first sweep;  nib : target syndrome bits
+//   FM   : 0 = `first_rt` read at run time, 1 = first sweep (compile time), 2 = not the first sweep.
+//          On a group's first sweep all messages are L = 0 (R16) and are not loaded.
 //   (A lane refilled alone has its bytes of the workspace reset to T = 192 when its frame is loaded.)
-//   PF   : while emitting, load the next row's (nx) message words into S as this row's words are
-//          stored, so the next row's global-memory latency overlaps this row's arithmetic.
-//   FM   : 0 = `first` read at run time, 1 = first sweep (compile time), 2 = not the first sweep.
+//   PF   : as soon as the gather has consumed S, load the next row's (nx) SW message words into it
+//          (positions beyond nx.D are harmless reads inside the workspace and its slack), so the next row's
+//          global-memory latency is hidden behind this row's arithmetic.
 template <int D, bool ESM, bool POW2, int KEEP_ADDR_MAX, bool PF, int FM, int SW>
 __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, uint32_t r4, uint32_t zm4,
                                            unsigned char* Eb, uint32_t* __restrict__ Lslot, int base, int r,
                                            uint32_t (&S)[SW], bool have, const NextRow nx, uint32_t nib,
                                            bool first_rt, const Konst& K) {
+    static_assert(SW >= D, "message register array");
     const bool first = FM == 1 || (FM == 0 && first_rt);
-    static_assert(SW % 4 == 0 && SW >= ((D + 3) & ~3) && (D % 4 == 0 || (D & ~3) <= SW - 4), "message register array");
-    constexpr int Q4 = D & ~3;
     // High degrees recompute each E address in the emit phase (one smem table load + IMAD + LOP3)
     // instead of holding D addresses in registers through the forward/backward passes.
     constexpr bool KEEP_ADDR = D <= KEEP_ADDR_MAX;
     // Degrees above 20 (the degree <= 32 kernel) keep only cw and the old message word per edge
     // between the gather and the emit (edge_out_s recomputes x from them): 2 registers per edge
-    // instead of 3, so rows up to degree 32 stay in registers.
+    // instead of 3, so rows up to degree 32 stay in registers.  (Their S words live until the emit,
+    // so they prefetch word by word after each emit.)
 #ifndef QKD_LOWREG_MIN
 #define QKD_LOWREG_MIN 21
 #endif
@@ -262,37 +238,43 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
     uint32_t addr[D];
     EdgeIn in[D];
     uint32_t P = 0;
+    const uint32_t* Lr = msg_row(Lslot, base, D, r);   // word q at Lr[32 q]
     if (first) {
 #pragma unroll
-        for (int q = 0; q < SW; ++q) S[q] = 0xC0C0C0C0u;
-    } else if (!have) {
-        msg_load(Lslot, base, D, Z, r, S, 0);
+        for (int q = 0; q < D; ++q) S[q] = 0xC0C0C0C0u;
+    } else {
+#pragma unroll
+        for (int q = 0; q < D; ++q)
+            if (!have || (PF && !LOWREG && q >= QKD_PF_WORDS)) S[q] = Lr[32 * q];
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) addr[k] = Addr<POW2>::at(et[k], r4, zm4, Z, K);
 #pragma unroll
-    for (int q = 0; q < D; ++q) {      // gather in emission order: the last-prefetched words last
+    for (int q = 0; q < D; ++q) {      // gather in emission order
         const int k = emit_edge(D, q);
-        in[k] = edge_in(ldE<ESM>(Eb, addr[k]), S[msg_slot<SW>(D, q)], K);
+        in[k] = edge_in(ldE<ESM>(Eb, addr[k]), S[q], K);
         P ^= in[k].cw;
+    }
+    const uint32_t* Ln = msg_row(Lslot, nx.base, nx.D, nx.r);
+    constexpr int NPF = SW < QKD_PF_WORDS ? SW : QKD_PF_WORDS;
+    if constexpr (PF && !LOWREG) {
+        if (nx.D > 0) {
+#pragma unroll
+            for (int q = 0; q < NPF; ++q) S[q] = Ln[32 * q];
+        }
     }
     // Eq.(1) with the target bit: L_new of edge k is negative iff
     // s_i ^ XOR_{j != k} [x_j < 0] = s_i ^ ((D-1)&1) ^ P ^ nonneg_k   (bit 6)
     const uint32_t Q = P ^ nib_to_bit6(nib) ^ (((D - 1) & 1) ? 0x40404040u : 0u);
-    // group g of this row at Lm + g 4Z, of the next row at Ln + g 4Z.  The pointers are opaque
-    // GENERIC pointers: ptxas keeps generic accesses in order with the row's shared-memory E
-    // accesses (they might alias), which pins each group store, and the next row's load into
-    // the registers it frees, where the source puts them -- with global pointers it sinks all of
-    // them to the end of the row and the prefetch hides nothing.
-    uint32_t *Lm, *Ln;
-    asm("mov.b64 %0, %1;" : "=l"(Lm) : "l"(Lslot + base + 4 * r));
-    if constexpr (PF) asm("mov.b64 %0, %1;" : "=l"(Ln) : "l"(Lslot + nx.base + 4 * nx.r));
-    const long long zs = 4LL * Z;
+    // an opaque GENERIC pointer: ptxas keeps generic stores in order with the row's shared-memory
+    // E accesses (they might alias), which pins each message store at its edge's emit; through a
+    // global pointer it sinks them all to the end of the row, holding D words in registers
+    uint32_t* Lw;
+    asm("mov.b64 %0, %1;" : "=l"(Lw) : "l"(msg_row(Lslot, base, D, r)));
     // emit edge k as soon as its leave-one-out magnitude is known (keeps the live set small); its
-    // message word sits at position q = emit_pos(D, k), and positions are emitted in increasing
-    // order, so a uint4 group is final (stored, then refilled with the next row's words) at q % 4 == 3
+    // new message word goes straight to position q = emit_pos(D, k)
     auto emit = [&](int k, uint32_t o) {
-        const int q = emit_pos(D, k), sl = msg_slot<SW>(D, q);
+        const int q = emit_pos(D, k);
         uint32_t a;
         if constexpr (KEEP_ADDR) {
             a = addr[k];
@@ -302,25 +284,17 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
             a = Addr<POW2>::at(e, r4, zm4, Z, K);
         }
         const uint32_t ew = ldE<ESM>(Eb, a);
-        uint32_t eo;
-        if constexpr (LOWREG)
-            S[sl] = edge_out_s(o, Q ^ in[k].cw, S[sl], ew, K, eo);
-        else
-            S[sl] = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
-        stE<ESM>(Eb, a, eo);
-        if (q < Q4 && (q & 3) == 3) {
-            const int g = q >> 2;
-            st4(Lm + g * zs, make_uint4(S[4 * g], S[4 * g + 1], S[4 * g + 2], S[4 * g + 3]));
-            if constexpr (PF) {   // the next row's group g into the registers just stored
-                if (4 * g < (nx.D & ~3)) {
-                    const uint4 v = ld4(Ln + g * zs);
-                    S[4 * g] = v.x; S[4 * g + 1] = v.y; S[4 * g + 2] = v.z; S[4 * g + 3] = v.w;
-                }
+        uint32_t eo, tn;
+        if constexpr (LOWREG) {
+            tn = edge_out_s(o, Q ^ in[k].cw, S[q], ew, K, eo);
+            if constexpr (PF) {
+                if (nx.D > 0) S[q] = Ln[32 * q];
             }
-        } else if ((D & 2) && q == Q4 + 1) {
-            *reinterpret_cast<uint2*>(Lslot + base + (long long)Z * Q4 + 2 * r) = make_uint2(S[SW - 4], S[SW - 3]);
+        } else {
+            tn = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
         }
-        if ((D & 1) && q == D - 1) Lslot[base + (long long)Z * (Q4 + (D & 2)) + r] = S[SW - 1];
+        stE<ESM>(Eb, a, eo);
+        Lw[32 * q] = tn;
     };
     // magnitudes in complement form (tau4c / edge_magc / edge_out_c): two instructions fewer per tau
 #define QKD_TAU tau4c
@@ -369,9 +343,6 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
 #undef QKD_TAU
 #undef QKD_MAG
 #undef QKD_O63
-    if constexpr (PF) {   // the next row's groups beyond this row's and its tail words
-        if (nx.D > 0) msg_load(Lslot, nx.base, nx.D, Z, nx.r, S, Q4 / 4);
-    }
 }
 
 // ---------------------------------------------------------------------------------------------

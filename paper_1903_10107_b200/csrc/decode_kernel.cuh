@@ -13,18 +13,28 @@
 namespace qkd {
 
 
+// the slot's named barrier; with one slot per CTA (e.g. C5a) the id is the immediate 1, so no
+// register holds it across the row updates (it was spilled and reloaded before every barrier)
+__device__ __forceinline__ void slot_bar(const DecParams& p, int bar) {
+    if (p.GPC == 1)
+        asm volatile("bar.sync 1, %0;" ::"r"(p.TG) : "memory");
+    else
+        group_bar(bar, p.TG);
+}
+
 #ifndef QKD_PF_DMAX
-#define QKD_PF_DMAX 0   // decode variant (DMAX) that prefetches the next row's messages (0: none, -1: all; measured slower on C5a: +6% SASS)
+#define QKD_PF_DMAX 0   // decode variant (DMAX) that prefetches the next row's messages (0: none, -1: all;
+                        // C5a: 52.7 ms without, 56.6 with (its 20 live words spill at 128 registers))
 #endif
 template <int DMAX, bool SPLIT>
 struct Prefetch {
     static constexpr bool on = !SPLIT && DMAX > 0 && (DMAX == QKD_PF_DMAX || QKD_PF_DMAX < 0);
 };
 
-// registers for one row's message words (decode.cuh msg_slot)
+// registers for one row's message words
 template <int DMAX>
 struct MsgRegs {
-    static constexpr int SW = DMAX > 0 ? ((DMAX + 3) & ~3) : 4;
+    static constexpr int SW = DMAX > 0 ? DMAX : 1;
 };
 
 // One layer (block row) of the slot's rows.  S/have: message words of this thread's next row,
@@ -142,7 +152,7 @@ __device__ __forceinline__ uint32_t syndrome_viol(const DecParams& p, const int4
     v &= 0x80808080u;
     v = __reduce_or_sync(0xffffffffu, v);
     if ((threadIdx.x & 31) == 0 && v) atomicOr(&flags[chk & 1], v);
-    group_bar(bar, p.TG);
+    slot_bar(p, bar);
     const uint32_t res = *(volatile uint32_t*)&flags[chk & 1];
     if (t == 0) flags[(chk + 1) & 1] = 0;   // next check's flag: last read before this barrier
     ++chk;
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
         auto refill_lanes = [&](uint32_t mask) -> uint32_t {
             const int k = __popc(mask);
             if (t == 0) ctl[0] = atomicAdd(p.work, k);
-            group_bar(bar, p.TG);
+            slot_bar(p, bar);
             const long long a = *(volatile int*)&ctl[0];
             long long fid[4];
             uint32_t got = 0;
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
                     sSyn[i] = (uint8_t)b;
                 }
             }
-            group_bar(bar, p.TG);
+            slot_bar(p, bar);
             return got;
         };
         auto finish = [&](uint32_t mask, uint32_t succ, uint32_t zeroL) {
@@ -340,7 +350,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
             int itv[4];
             lane_state(fr, itv);
             finalize(p, s_layer, Eslot, Lslot, fr, mask, itv, succ, zeroL, t);
-            group_bar(bar, p.TG);
+            slot_bar(p, bar);
         };
         if (t == 0) { flags[0] = 0; flags[1] = 0; }
         uint32_t pend = refill_lanes(0xFu);
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
                 const int4 li = s_layer[I];
                 layer_pass<DMAX, ESM, POW2, SPLIT, false>(p, li, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,
                                                           fresh == 0xFu ? 0xFu : 0u, S, have, K);
-                group_bar(bar, p.TG);
+                slot_bar(p, bar);
             }
             ++sweeps;
             fresh = 0;
@@ -400,7 +410,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
     } else {
     for (;;) {   // whole 4-frame groups: a slot takes the next 4 frames when all of its lanes stop
         if (t == 0) ctl[0] = atomicAdd(p.work, 1);
-        group_bar(bar, p.TG);
+        slot_bar(p, bar);
         const long long g = *(volatile int*)&ctl[0];
         if (g >= p.ngroups) break;
         const long long f0 = g * kFramesPerGroup;
@@ -456,7 +466,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
             flags[0] = 0;
             flags[1] = 0;
         }
-        group_bar(bar, p.TG);
+        slot_bar(p, bar);
 
         uint32_t active = (1u << nl) - 1u;
         int chk = 0;
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
             const uint32_t done = active & ~viol;
             if (done) {
                 fin(done, 0, done, 0xFu);
-                group_bar(bar, p.TG);
+                slot_bar(p, bar);
             }
             active &= viol;
         }
@@ -479,7 +489,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
         layer_pass<DMAX, ESM, POW2, SPLIT, Prefetch<DMAX, SPLIT>::on, FM>(                               \
             p, li, lin, SPLIT ? s_edge2 + s_soff[I] : s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,       \
             FM == 1 ? 0xFu : 0u, S, have, K);                                                            \
-        group_bar(bar, p.TG);                                                                            \
+        slot_bar(p, bar);                                                                            \
     }
         while (active && it < p.T) {
             ++it;
@@ -494,7 +504,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
                 const uint32_t done = active & ~viol;
                 if (done) {
                     fin(done, it, done, 0u);
-                    group_bar(bar, p.TG);
+                    slot_bar(p, bar);
                 }
                 active &= viol;
             }
@@ -505,7 +515,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
                 succ = active & ~syndrome_viol<DMAX, ESM, POW2>(p, s_layer, s_edge, Eb, sSyn, t, flags, chk, bar, K, active);
             fin(active, it, succ, it == 0 ? 0xFu : 0u);
         }
-        group_bar(bar, p.TG);
+        slot_bar(p, bar);
     }
     }
 }

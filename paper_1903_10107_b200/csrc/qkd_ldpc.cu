@@ -441,7 +441,9 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     const long long ctas = (pl.ngroups + gpc - 1) / gpc;
     pl.grid = (int)std::max<long long>(1, std::min<long long>(ctas, (long long)per_sm * di.sms));
     pl.slots = (long long)pl.grid * gpc;
-    pl.ws_L = (size_t)pl.slots * (size_t)c->ws_words * 4;
+    // + slack after the last slot: the message prefetch reads up to 32 positions of a thread's next
+    // row whatever its degree (decode.cuh row_update), i.e. up to 32 x 32 words past a row chunk
+    pl.ws_L = ((size_t)pl.slots * (size_t)c->ws_words + 32 * 32) * 4;
     pl.ws_E = gE ? (size_t)pl.slots * (size_t)c->n * 4 : 0;
     pl.ws_total = 256 + pl.ws_L + pl.ws_E;
     return QKD_OK;
@@ -515,8 +517,9 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
             li.w = li.x;
         }
         li.z = (int)c->ws_words;
-        c->ws_words += (int64_t)Z * li.w;
-        c->ws_words = (c->ws_words + 3) & ~3LL;   // every block row's regions start 16-byte aligned
+        // lane-pair layout: Z rows of li.w words; otherwise 32-row chunks of li.w = D words (msg_word)
+        c->ws_words += (c->split ? (int64_t)Z : ((int64_t)Z + 31) / 32 * 32) * li.w;
+        c->ws_words = (c->ws_words + 3) & ~3LL;   // 16-byte aligned block rows (lane-pair layout: 64-bit moves)
         if (c->ws_words > (1LL << 31) - 1) {
             delete c;
             return fail(QKD_EUNSUP, "code too large for the 32-bit workspace offsets");

@@ -47,6 +47,13 @@ __device__ __forceinline__ uint32_t rep4(uint32_t byte) { return byte * 0x010101
 
 // a*m + c on the FMA pipe
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t m, uint32_t c) { return a * m + c; }
+// a*M + c with an immediate multiplier (|M| != 1: ptxas keeps these as IMAD, no constant register)
+template <int M>
+__device__ __forceinline__ uint32_t imadi(uint32_t a, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "n"(M), "r"(c));
+    return r;
+}
 // LOP3 with an explicit truth table (a = 0xF0, b = 0xCC, c = 0xAA).  Written as PTX so ptxas does
 // not fold a NOT into a neighbouring add (it rewrites ~(d + k) as -d - k - 1, costing a negate).
 template <uint32_t LUT>
@@ -117,7 +124,11 @@ __device__ __forceinline__ uint32_t lo16s(uint32_t w) { return prmt<0xA280u>(w, 
 // pack the low bytes of two 16x2 words back into frame order {0,1,2,3}
 __device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi) { return prmt<0x6240u>(lo, hi); }
 // the same for clean lanes (every 16-bit lane in [0, 255]) on the FMA pipe: lo + 256 hi
-__device__ __forceinline__ uint32_t pack16c(uint32_t lo, uint32_t hi, const Konst& K) { return imad(hi, K.p256, lo); }
+__device__ __forceinline__ uint32_t pack16c(uint32_t lo, uint32_t hi, const Konst& K) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, 256, %2;" : "=r"(r) : "r"(hi), "r"(lo));
+    return r;
+}
 // byte mask 0xFF where bit 7 of the byte is set
 __device__ __forceinline__ uint32_t bmask7(uint32_t w) { return prmt<0xBA98u>(w, 0u); }
 
