@@ -102,6 +102,12 @@ __device__ __forceinline__ EdgeIn edge_in(uint32_t e, uint32_t tw, const Konst& 
     r.cw = pack16c(clo, chi, K);      // bytes in [0, 126]; bit 6 = (x >= 1) -- x = 0 counts as
     return r;                         // negative, which is immaterial (R23)
 }
+// The output sign of Eq.(1) for edge k at bit 7 of each byte: Q2 = 2 (Q & 0x40404040), Q = the row's
+// sign product (bit 6, target bit included), cw = the edge's clamp word (sign of x at bit 6).  As an
+// add, 2 (Q6 + cw): bit 6 of Q6 + cw is Q6 ^ cw (Q6 has no low bits, so nothing carries into bit 6),
+// doubled it sits at bit 7; the carry out of a byte only sets bit 0 of the next (an even value + 1),
+// never its bit 7.  One IMAD instead of an XOR and a shift.
+__device__ __forceinline__ uint32_t sign_s7(uint32_t Q2, uint32_t cw) { return imadi<2>(cw, Q2); }
 // check-node magnitude min(|x|, 63) (MSG_max = 63)
 __device__ __forceinline__ uint32_t edge_mag(uint32_t cw, const Konst& K) { return __vabsdiffu4(cw, K.c63); }
 
@@ -120,9 +126,9 @@ __device__ __forceinline__ uint32_t edge_magc_alt(uint32_t cw) { return 0x3F3F3F
 //   E_new'' = clamp(ew + T_new - T_old, 0, 254) = clamp(E + L_new - L_old, -127, 127) + 127,
 // with d = T_new - T_old + 128 in [2, 254] per byte and the sum in 16-bit lanes; Algorithm 2
 // keeps ew where |E| = 127.  Returns T_new.
-__device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t negf, uint32_t t_old, uint32_t ew,
+__device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t s7, uint32_t t_old, uint32_t ew,
                                                const Konst& K, uint32_t& e_out) {
-    const uint32_t M = bmask7(imadi<2>(negf, 0u));             // 0xFF where L_new < 0
+    const uint32_t M = bmask7(s7);                                // 0xFF where L_new < 0
     const uint32_t nx = lop3i<0x87, 0x7F7F7F7Fu>(oc, M);          // ~(oc ^ (M & 0x7F))
     const uint32_t sn = imad(lop3i<0xA0, 0x01010101u>(M, 0u), K.one, nx);   // + (M & 1)
     const uint32_t d = sn - t_old + 0x80808080u;                  // IADD3, exact per byte
@@ -134,12 +140,12 @@ __device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t negf, uint3
     return sn;
 }
 
-// Given the leave-one-out magnitude o, the sign flag (bit 6 of negf = 1 -> L_new < 0), the
+// Given the leave-one-out magnitude o, the sign flag (bit 7 of s7 = 1 -> L_new < 0; sign_s7 below), the
 // edge's X words and the pre-layer E word: returns the new S word (stored) and writes the new
 // E word (Algorithm 2 guard on |E| = E_max, Eq.(9) saturated to +-127).
-__device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t negf, const EdgeIn& in, uint32_t ew,
+__device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t s7, const EdgeIn& in, uint32_t ew,
                                              const Konst& K, uint32_t& e_out) {
-    const uint32_t M = bmask7(imadi<2>(negf, 0u));             // 0xFF where L_new < 0
+    const uint32_t M = bmask7(s7);                                // 0xFF where L_new < 0
     const uint32_t om = o & M;
     const uint32_t Tb = imad(om, K.m2, imad(o, K.one, 0xC0C0C0C0u));   // bytes (64 + L_new) + 128
     const uint32_t thi = hi16s(Tb);                               // lanes {1,3}: 64 + L_new - 128
@@ -153,13 +159,19 @@ __device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t negf, const Ed
 
 // edge_out with the leave-one-out magnitude in complement form oc = 63 - o (tau4c output):
 // o & M = (oc ^ 63) & M is still one LOP3 and o + 0xC0 = 0xFF - oc one IMAD, so nothing is added.
-__device__ __forceinline__ uint32_t edge_out_c(uint32_t oc, uint32_t negf, const EdgeIn& in, uint32_t ew,
+__device__ __forceinline__ uint32_t edge_out_c(uint32_t oc, uint32_t s7, const EdgeIn& in, uint32_t ew,
                                                const Konst& K, uint32_t& e_out) {
-    const uint32_t M = bmask7(imadi<2>(negf, 0u));             // 0xFF where L_new < 0
+    const uint32_t M = bmask7(s7);                                // 0xFF where L_new < 0
     const uint32_t om = lop3i<0x48, 0x3F3F3F3Fu>(oc, M);          // (oc ^ 63) & M = o & M
     const uint32_t Tb = imadi<-2>(om, imad(oc, K.m1, 0xFFFFFFFFu));   // 255 - oc - 2 om = 192 + L_new
     const uint32_t thi = hi16s(Tb);                               // lanes {1,3}: L_new - 64
+#ifndef QKD_TLO_IMAD   // the FMA-pipe form below measured 0.6% slower on C5a
     const uint32_t tlo = lo16s(Tb);                               // lanes {0,2}: L_new - 64
+#else
+    // lanes {0,2} on the FMA pipe: Tb + 0xFFFFFF00 - 256 thi = (b0 - 256, b2 - 256) for bytes with
+    // bit 7 set (the identity edge_out uses)
+    const uint32_t tlo = imadi<-256>(thi, imad(Tb, K.one, 0xFFFFFF00u));
+#endif
     const uint32_t enew = pack16c(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu), K);
     const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);
@@ -186,7 +198,9 @@ __device__ __forceinline__ uint32_t& w4(uint4& v, int i) { return i == 0 ? v.x :
 // to one position is 128 contiguous bytes, a thread's words are at immediate offsets 128 q from
 // one pointer, no padding word is ever moved (write traffic = the algorithmic bytes), a row's
 // words are stored one by one as they are emitted (nothing buffered in registers for a vector
-// store) and the next row's words can be loaded as soon as this row's gather has consumed its own.
+// store).  (Loading the next row's words early -- after this row's gather, late in its emit, or
+// before the block-row barrier -- was measured slower on C5a, 57-61 vs 52.8 ms: every form keeps
+// extra words live across code ptxas then schedules worse.)
 __host__ __device__ constexpr int emit_pos(int D, int k) {    // emission step of edge k
     return k >= D / 2 ? 2 * (k - D / 2) : 2 * (D / 2 - 1 - k) + 1;
 }
@@ -200,53 +214,33 @@ __device__ __forceinline__ uint32_t* msg_row(uint32_t* Lslot, int base, int D, i
 __device__ __forceinline__ uint32_t* msg_word(uint32_t* Lslot, int base, int D, int Z, int r, int q) {
     return msg_row(Lslot, base, D, r) + 32 * q;
 }
-#ifndef QKD_PF_WORDS
-#define QKD_PF_WORDS 32   // prefetch at most this many positions (the rest load at the row's start)
-#endif
-// the thread's next row (message prefetch target): degree D (0 = none), block-row base, row
-struct NextRow {
-    int base, D, r;
-};
-
 // One check row r of a block row with D edges (layered update, Alg. 1/2).
-//   et   : the row's D (cb, s) entries;  S : the row's message words (emission order), loaded here
-//          unless `have` (prefetched by the previous row) or the first sweep;  nib : target syndrome bits
+//   et   : the row's D (cb, s) entries;  nib : target syndrome bits
 //   FM   : 0 = `first_rt` read at run time, 1 = first sweep (compile time), 2 = not the first sweep.
 //          On a group's first sweep all messages are L = 0 (R16) and are not loaded.
 //   (A lane refilled alone has its bytes of the workspace reset to T = 192 when its frame is loaded.)
-//   PF   : as soon as the gather has consumed S, load the next row's (nx) SW message words into it
-//          (positions beyond nx.D are harmless reads inside the workspace and its slack), so the next row's
-//          global-memory latency is hidden behind this row's arithmetic.
-template <int D, bool ESM, bool POW2, int KEEP_ADDR_MAX, bool PF, int FM, int SW>
+template <int D, bool ESM, bool POW2, int KEEP_ADDR_MAX, int FM>
 __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, uint32_t r4, uint32_t zm4,
                                            unsigned char* Eb, uint32_t* __restrict__ Lslot, int base, int r,
-                                           uint32_t (&S)[SW], bool have, const NextRow nx, uint32_t nib,
-                                           bool first_rt, const Konst& K) {
-    static_assert(SW >= D, "message register array");
+                                           uint32_t nib, bool first_rt, const Konst& K) {
     const bool first = FM == 1 || (FM == 0 && first_rt);
     // High degrees recompute each E address in the emit phase (one smem table load + IMAD + LOP3)
     // instead of holding D addresses in registers through the forward/backward passes.
     constexpr bool KEEP_ADDR = D <= KEEP_ADDR_MAX;
     // Degrees above 20 (the degree <= 32 kernel) keep only cw and the old message word per edge
     // between the gather and the emit (edge_out_s recomputes x from them): 2 registers per edge
-    // instead of 3, so rows up to degree 32 stay in registers.  (Their S words live until the emit,
-    // so they prefetch word by word after each emit.)
+    // instead of 3, so rows up to degree 32 stay in registers.
 #ifndef QKD_LOWREG_MIN
 #define QKD_LOWREG_MIN 21
 #endif
     constexpr bool LOWREG = D >= QKD_LOWREG_MIN;
     uint32_t addr[D];
     EdgeIn in[D];
+    uint32_t S[D];                                 // the row's message words, emission order
     uint32_t P = 0;
     const uint32_t* Lr = msg_row(Lslot, base, D, r);   // word q at Lr[32 q]
-    if (first) {
 #pragma unroll
-        for (int q = 0; q < D; ++q) S[q] = 0xC0C0C0C0u;
-    } else {
-#pragma unroll
-        for (int q = 0; q < D; ++q)
-            if (!have || (PF && !LOWREG && q >= QKD_PF_WORDS)) S[q] = Lr[32 * q];
-    }
+    for (int q = 0; q < D; ++q) S[q] = first ? 0xC0C0C0C0u : Lr[32 * q];
 #pragma unroll
     for (int k = 0; k < D; ++k) addr[k] = Addr<POW2>::at(et[k], r4, zm4, Z, K);
 #pragma unroll
@@ -255,17 +249,10 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         in[k] = edge_in(ldE<ESM>(Eb, addr[k]), S[q], K);
         P ^= in[k].cw;
     }
-    const uint32_t* Ln = msg_row(Lslot, nx.base, nx.D, nx.r);
-    constexpr int NPF = SW < QKD_PF_WORDS ? SW : QKD_PF_WORDS;
-    if constexpr (PF && !LOWREG) {
-        if (nx.D > 0) {
-#pragma unroll
-            for (int q = 0; q < NPF; ++q) S[q] = Ln[32 * q];
-        }
-    }
     // Eq.(1) with the target bit: L_new of edge k is negative iff
     // s_i ^ XOR_{j != k} [x_j < 0] = s_i ^ ((D-1)&1) ^ P ^ nonneg_k   (bit 6)
     const uint32_t Q = P ^ nib_to_bit6(nib) ^ (((D - 1) & 1) ? 0x40404040u : 0u);
+    const uint32_t Q2 = (Q & 0x40404040u) << 1;
     // an opaque GENERIC pointer: ptxas keeps generic stores in order with the row's shared-memory
     // E accesses (they might alias), which pins each message store at its edge's emit; through a
     // global pointer it sinks them all to the end of the row, holding D words in registers
@@ -286,12 +273,9 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
         const uint32_t ew = ldE<ESM>(Eb, a);
         uint32_t eo, tn;
         if constexpr (LOWREG) {
-            tn = edge_out_s(o, Q ^ in[k].cw, S[q], ew, K, eo);
-            if constexpr (PF) {
-                if (nx.D > 0) S[q] = Ln[32 * q];
-            }
+            tn = edge_out_s(o, sign_s7(Q2, in[k].cw), S[q], ew, K, eo);
         } else {
-            tn = edge_out_c(o, Q ^ in[k].cw, in[k], ew, K, eo);
+            tn = edge_out_c(o, sign_s7(Q2, in[k].cw), in[k], ew, K, eo);
         }
         stE<ESM>(Eb, a, eo);
         Lw[32 * q] = tn;
@@ -394,7 +378,7 @@ __device__ __forceinline__ void row_update_split(const int2* __restrict__ et2, i
         const uint32_t aj = addr(j);
         const uint32_t ew = ldE<true>(Eb, aj);        // pre-layer E (no other row of the layer touches it)
         uint32_t eo;
-        const uint32_t sn = edge_out_s(oc, Q ^ cw[j], sw(j), ew, K, eo);
+        const uint32_t sn = edge_out_s(oc, sign_s7((Q & 0x40404040u) << 1, cw[j]), sw(j), ew, K, eo);
         sw(j) = sn;
         if (act) {
             stE<true>(Eb, aj, eo);
@@ -474,7 +458,7 @@ __device__ __noinline__ void row_update_generic(const int2* __restrict__ et, int
     for (int k = 0; k < D; ++k) {
         const uint32_t ew = ldE<ESM>(Eb, addr[k]);
         uint32_t eo;
-        *wp[k] = edge_out(o[k], Q ^ in[k].cw, in[k], ew, K, eo);
+        *wp[k] = edge_out(o[k], sign_s7((Q & 0x40404040u) << 1, in[k].cw), in[k], ew, K, eo);
         stE<ESM>(Eb, addr[k], eo);
     }
 }

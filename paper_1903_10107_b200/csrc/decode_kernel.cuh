@@ -22,29 +22,11 @@ __device__ __forceinline__ void slot_bar(const DecParams& p, int bar) {
         group_bar(bar, p.TG);
 }
 
-#ifndef QKD_PF_DMAX
-#define QKD_PF_DMAX 0   // decode variant (DMAX) that prefetches the next row's messages (0: none, -1: all;
-                        // C5a: 52.7 ms without, 56.6 with (its 20 live words spill at 128 registers))
-#endif
-template <int DMAX, bool SPLIT>
-struct Prefetch {
-    static constexpr bool on = !SPLIT && DMAX > 0 && (DMAX == QKD_PF_DMAX || QKD_PF_DMAX < 0);
-};
-
-// registers for one row's message words
-template <int DMAX>
-struct MsgRegs {
-    static constexpr int SW = DMAX > 0 ? DMAX : 1;
-};
-
-// One layer (block row) of the slot's rows.  S/have: message words of this thread's next row,
-// prefetched by the previous row when PF (kept across block rows and the block-row barrier:
-// a row's messages are only ever written by the thread that owns the row).  lin = the next
-// block row's layer entry (prefetch target after this block row's last row).
-template <int DMAX, bool ESM, bool POW2, bool SPLIT, bool PF, int FM = 0>
-__device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, const int4 lin, const int2* et, int t,
+// One layer (block row) of the slot's rows.
+template <int DMAX, bool ESM, bool POW2, bool SPLIT, int FM = 0>
+__device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, const int2* et, int t,
                                            unsigned char* Eb, uint32_t* Lslot, const uint8_t* synI, uint32_t fresh,
-                                           uint32_t (&S)[MsgRegs<DMAX>::SW], bool& have, const Konst& K) {
+                                           const Konst& K) {
     const bool first = fresh == 0xFu;   // all four lanes on their first sweep: L = 0 without loading
     const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
     if (li.x == 0) return;              // a check row with no variables: nothing to update (oracle: no-op)
@@ -76,13 +58,9 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
 #define QKD_CASE(DD)                                                                                     \
     case DD:                                                                                             \
         if constexpr (DD <= DMAX) {                                                                      \
-            for (int r = t; r < p.Z; r += p.TG) {                                                        \
-                const bool more = r + p.TG < p.Z;                                                        \
-                const NextRow nx{more ? li.z : lin.z, PF ? (more ? DD : lin.x) : 0, more ? r + p.TG : t}; \
-                row_update<DD, ESM, POW2, (DMAX <= 8 ? 4 : QKD_KEEP_ADDR), PF, FM>(et, p.Z, 4u * r, zm4, Eb, Lslot, li.z, r, \
-                                                                               S, have, nx, synI[r], first, K); \
-                have = PF && nx.D > 0;                                                                   \
-            }                                                                                            \
+            for (int r = t; r < p.Z; r += p.TG)                                                          \
+                row_update<DD, ESM, POW2, (DMAX <= 8 ? 4 : QKD_KEEP_ADDR), FM>(et, p.Z, 4u * r, zm4, Eb, Lslot,   \
+                                                                               li.z, r, synI[r], first, K);     \
             return;                                                                                      \
         }                                                                                                \
         break;
@@ -258,8 +236,6 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
     int* ctl = reinterpret_cast<int*>(sSyn + ((p.m + 15) & ~15));   // [0] group id, [1..2] flags
     uint32_t* flags = reinterpret_cast<uint32_t*>(ctl + 1);
     uint32_t* Lslot = p.Lws + gslot * p.ws_words;
-    uint32_t S[MsgRegs<DMAX>::SW];   // this thread's next row's message words (prefetched when Prefetch::on)
-    bool have = false;
 
     if constexpr (!SPLIT && REFILL) {
         // ---- per-frame scheduling: a lane whose frame stops is refilled with the next frame at
@@ -389,8 +365,8 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
             if (!active) break;
             for (int I = 0; I < p.Mb; ++I) {   // idle lanes (no frame left) compute harmlessly
                 const int4 li = s_layer[I];
-                layer_pass<DMAX, ESM, POW2, SPLIT, false>(p, li, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,
-                                                          fresh == 0xFu ? 0xFu : 0u, S, have, K);
+                layer_pass<DMAX, ESM, POW2, SPLIT>(p, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,
+                                                   fresh == 0xFu ? 0xFu : 0u, K);
                 slot_bar(p, bar);
             }
             ++sweeps;
@@ -485,11 +461,9 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
 #define QKD_SWEEP(FM)                                                                                    \
     for (int I = 0; I < p.Mb; ++I) {                                                                     \
         const int4 li = s_layer[I];                                                                      \
-        const int4 lin = s_layer[I + 1 < p.Mb ? I + 1 : 0];                                              \
-        layer_pass<DMAX, ESM, POW2, SPLIT, Prefetch<DMAX, SPLIT>::on, FM>(                               \
-            p, li, lin, SPLIT ? s_edge2 + s_soff[I] : s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,       \
-            FM == 1 ? 0xFu : 0u, S, have, K);                                                            \
-        slot_bar(p, bar);                                                                            \
+        layer_pass<DMAX, ESM, POW2, SPLIT, FM>(p, li, SPLIT ? s_edge2 + s_soff[I] : s_edge + li.y, t, Eb,   \
+                                               Lslot, sSyn + I * p.Z, FM == 1 ? 0xFu : 0u, K);          \
+        slot_bar(p, bar);                                                                                \
     }
         while (active && it < p.T) {
             ++it;

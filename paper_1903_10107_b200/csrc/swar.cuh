@@ -102,7 +102,11 @@ __device__ __forceinline__ uint32_t tau4(uint32_t a, uint32_t b, const Konst& K)
 //   c = [l>=3]([d<2] + [d<6]) + [1<=l<=2][d<4]  as above.
 __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K) {
     const uint32_t d = __vabsdiffu4(a, b);                       // ALU
+#if QKD_TAU_IMAD
+    const uint32_t g = imad(a, K.one, imad(b, K.one, d)) >> 1;   // 2 IMAD + SHF (experiment)
+#else
     const uint32_t g = (a + b + d) >> 1;                         // IADD3 + SHF (a+b+d = 2 max <= 126)
+#endif
     const uint32_t p = imad(g, K.one, 0x03030303u);              // bit6: l <= 2
     const uint32_t z = imad(g, K.one, 0x01010101u);              // bit6: l == 0
     const uint32_t U = imad(d, K.one, 0x3E3E3E3Eu);              // bit6: d >= 2
