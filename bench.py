@@ -212,7 +212,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
-            "data": "synthetic", "config": workload_config(args.workload),
+            "data": "synthetic", "config": workload_config(args.workload, args.gpus, args.scaling),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": sample_desc + " per step, extrapolated to the full workload"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -220,7 +220,19 @@ def run_reference(args):
     return 0
 
 
-def workload_config(wl):
+def workload_efficiency(name):
+    """R20: f = (m - p) / ((n - p - s) h2(q)) of a workload (the reference it is quoted against)."""
+    import math
+
+    w = synth.workload(name)
+    d, p, s = w.rate_adaptive_counts()
+    q = w.qber
+    h2 = -q * math.log2(q) - (1 - q) * math.log2(1 - q)
+    return (w.m - p) / ((w.n - p - s) * h2)
+
+
+def workload_config(wl, gpus=1, scaling="strong"):
+    """The config dict -- identical in both arms (native and --impl reference)."""
     names = WORKLOADS[wl]
     cfg = {"workload": wl + " = " + " + ".join(
         f"{n}({synth.workload(n).Mb}x{synth.workload(n).Nb} Z={synth.workload(n).Z} n={synth.workload(n).n} "
@@ -229,58 +241,71 @@ def workload_config(wl):
         "frames_per_workload": {n: synth.workload(n).frames for n in names},
         "max_iter": {n: synth.workload(n).max_iter for n in names},
         "early_stop": True, "frames_per_group": 4,
+        "efficiency_f": {n: round(workload_efficiency(n), 4) for n in names},
+        "parallelism": f"frames sharded over {gpus} rank(s), {scaling} scaling",
         "l2": "inputs larger than L2 (C5a LLR alone is 3.4 GB); no flush needed"}
     return cfg
 
 
 # ------------------------------------------------------------------------------- GPU arm
-def run_gpu(args):
-    import torch
-    import torch.distributed as dist
+class NativeEngine:
+    """The product: this rank's shard of every workload decoded by libqkdldpc.so on its GPU.
+    The rank/step/timing control flow around it (run_ranks) is shared with the CPU test stub
+    (tests/bench_stub.py), which is how the multi-rank path is tested without GPUs."""
 
-    import paper_1903_10107_b200 as qkd
+    backend = "nccl"
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream()
-    names = WORKLOADS[args.workload]
-    nthreads = max(1, host_cores() // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    def __init__(self, args, world, rank, local):
+        import torch
 
-    # ---- per-workload state (this rank's shard of global frame ids)
-    W = []
-    for name in names:
-        w = synth.workload(name)
-        F = w.frames * (world if args.scaling == "weak" else 1)   # weak: BASELINE's count on every rank
-        a, b = shard(F, rank, world)
-        t0 = time.perf_counter()
-        x, y, _ = w.gen(a, b - a, nthreads)
-        kind = w.pos_kind()
-        code = qkd.QCCode(w.shifts(), w.Z, kind)
-        Fr = b - a
-        st = dict(name=name, w=w, code=code, F=Fr, x_host=x, y_host=y,
-                  x=torch.from_numpy(x).to(dev), y=torch.from_numpy(y).to(dev))
-        st["syn"] = torch.empty((Fr, code.mb8), dtype=torch.uint8, device=dev)
-        st["llr"] = torch.empty((Fr, code.n), dtype=torch.int8, device=dev)
-        st["ws"] = torch.empty(code.workspace_bytes(Fr), dtype=torch.uint8, device=dev)
-        st["out"] = dict(bits=torch.empty((Fr, code.nb8), dtype=torch.uint8, device=dev),
-                         iters=torch.empty(Fr, dtype=torch.int32, device=dev),
-                         success=torch.empty(Fr, dtype=torch.uint8, device=dev))
-        st["info"] = code.launch_info(Fr)
-        st["known"] = st["x"] if kind is not None else None
-        log(f"[rank {rank}] {name}: frames [{a},{b}) generated in {time.perf_counter() - t0:.1f}s, "
-            f"launch {st['info']}")
-        W.append(st)
-    counters = torch.zeros((len(W), 5), dtype=torch.int64, device=dev)
-    ev = {s["name"]: [] for s in W}
+        import paper_1903_10107_b200 as qkd
 
-    def step(record):
+        self.torch, self.qkd, self.args = torch, qkd, args
+        self.world, self.rank, self.local = world, rank, local
+        torch.cuda.set_device(local)
+        self.dev = torch.device("cuda", local)
+        self.stream = torch.cuda.current_stream()
+        self.device_id = self.dev
+
+    def prepare(self):
+        torch, qkd, args, dev = self.torch, self.qkd, self.args, self.dev
+        world, rank = self.world, self.rank
+        nthreads = max(1, host_cores() // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+        W = []
+        for name in WORKLOADS[args.workload]:
+            w = synth.workload(name)
+            F = w.frames * (world if args.scaling == "weak" else 1)   # weak: BASELINE's count on every rank
+            a, b = shard(F, rank, world)
+            t0 = time.perf_counter()
+            x, y, _ = w.gen(a, b - a, nthreads)
+            kind = w.pos_kind()
+            code = qkd.QCCode(w.shifts(), w.Z, kind)
+            Fr = b - a
+            st = dict(name=name, w=w, code=code, F=Fr, x_host=x, y_host=y,
+                      x=torch.from_numpy(x).to(dev), y=torch.from_numpy(y).to(dev))
+            st["syn"] = torch.empty((Fr, code.mb8), dtype=torch.uint8, device=dev)
+            st["llr"] = torch.empty((Fr, code.n), dtype=torch.int8, device=dev)
+            st["ws"] = torch.empty(code.workspace_bytes(Fr), dtype=torch.uint8, device=dev)
+            st["out"] = dict(bits=torch.empty((Fr, code.nb8), dtype=torch.uint8, device=dev),
+                             iters=torch.empty(Fr, dtype=torch.int32, device=dev),
+                             success=torch.empty(Fr, dtype=torch.uint8, device=dev))
+            st["info"] = code.launch_info(Fr)
+            st["known"] = st["x"] if kind is not None else None
+            st["ev"] = []
+            log(f"[rank {rank}] {name}: frames [{a},{b}) generated in {time.perf_counter() - t0:.1f}s, "
+                f"launch {st['info']}")
+            W.append(st)
+        self.W = W
+        self.launches_per_step = 4 * len(W)   # syndrome, LLR, decode, score per workload
+        return [s["name"] for s in W]
+
+    def zeros(self, shape):
+        return self.torch.zeros(shape, dtype=self.torch.int64, device=self.dev)
+
+    def step(self, counters, record):
+        torch, stream = self.torch, self.stream
         counters.zero_()
-        for i, s in enumerate(W):
+        for i, s in enumerate(self.W):
             code = s["code"]
             code.syndrome(s["x"], out=s["syn"])                       # Alice (a3)
             code.build_llr(s["w"].qber, s["y"], s["known"], out=s["llr"])   # Bob (a2)
@@ -291,88 +316,84 @@ def run_gpu(args):
                         out=s["out"])                                  # a4-a8
             e1.record(stream)
             if record:
-                ev[s["name"]].append((e0, e1))
+                s["ev"].append((e0, e1))
             code.score(s["out"]["bits"], s["x"], s["out"]["success"], counters=counters[i])   # a9
-        reduce_counters(counters, world)                              # a9: the only collective
 
-    for _ in range(args.warmup):
-        step(False)
-    torch.cuda.synchronize()
-    for v in ev.values():
-        v.clear()
-    clk = ClockSampler(local)
-    clk.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for _ in range(args.steps):
-        step(True)
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = clk.stop()
-    ms_local = t_start.elapsed_time(t_end)
-    ms = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_total = float(ms.item())
-    c = counters.cpu().numpy()      # last step (identical every step)
+    def sync(self):
+        self.torch.cuda.synchronize()
 
-    # ---- metric: corrected = syndrome matched and no payload bit error
-    corrected_bits = sum(int(c[i, 1] - c[i, 3]) * payload_bits(s["w"]) for i, s in enumerate(W))
-    processed_bits = sum(int(c[i, 0]) * payload_bits(s["w"]) for i, s in enumerate(W))
-    sec_per_step = ms_total / 1000.0 / args.steps
-    value = corrected_bits / sec_per_step / 1e6
-    processed = processed_bits / sec_per_step / 1e6
+    def clear_records(self):
+        for s in self.W:
+            s["ev"].clear()
 
-    # ---- roofline of the decode kernel (algorithmic bytes per launch / event time)
-    peak, peak_kind = peaks()
-    per_wl = {}
-    for i, s in enumerate(W):
-        code = s["code"]
-        t = statistics.mean(a.elapsed_time(b) for a, b in ev[s["name"]])
-        # this rank's algorithmic bytes: per frame-iteration 2|E| (every int8
-        # message read and rewritten once), per frame once n + ceil(m/8) + ceil(n/8) + 5.
-        frames_g, iters_g = int(c[i, 0]), int(c[i, 4])
-        frac = s["F"] / max(1, frames_g)
-        b_it = 2 * code.n_edges
-        once = code.n + code.mb8 + code.nb8 + 5
-        bytes_rank = frac * (iters_g * b_it + frames_g * once)
-        per_wl[s["name"]] = {"decode_ms": t, "alg_bytes": bytes_rank, "frames": frames_g,
-                             "fer": 1 - c[i, 1] / max(1, frames_g), "mean_iters": iters_g / max(1, frames_g),
-                             "undetected": int(c[i, 3]), "frames_with_errors": int(c[i, 2]),
-                             "alg_GBps": bytes_rank / (t / 1000) / 1e9, "launch": s["info"]}
-    dom = max(per_wl, key=lambda k: per_wl[k]["decode_ms"])
-    achieved = per_wl[dom]["alg_GBps"]
-    traffic, ncu = None, None
-    try:   # from the committed ncu capture of this launch (profiles/<tag>_decode_full.md)
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tj = json.load(f)
-        if tj.get("workload", "C5a") != dom:   # the capture is of another workload's launch
-            raise LookupError
-        traffic = tj.get("decode_dram_bytes_per_launch")
-        ncu = dict(tj.get("ncu") or {}, source=tj.get("source"))
-        if world > 1:   # the capture is of the 1-GPU launch (all frames of the workload)
-            traffic = None
-        elif ncu.get("warp_instructions") and clocks and clocks.get("sm_mhz"):
-            # SURVEY §8(d) co-bound: integer-issue fraction inst_executed / (SMs * 4 * clk * t), with the
-            # captured launch's instruction count (deterministic for this workload) and the live time/clock
-            sms = torch.cuda.get_device_properties(dev).multi_processor_count
-            ncu["int_issue_frac_live"] = ncu["warp_instructions"] / (
-                sms * 4 * clocks["sm_mhz"] * 1e6 * per_wl[dom]["decode_ms"] / 1000)
-    except Exception:
-        pass
+    def start_timer(self):
+        self.t_start = self.torch.cuda.Event(enable_timing=True)
+        self.t_end = self.torch.cuda.Event(enable_timing=True)
+        self.clk = ClockSampler(self.local)
+        self.clk.start()
+        self.t_start.record(self.stream)
 
-    # ---- end to end through the C ABI with host buffers (pinned), N GPUs
-    e2e = run_e2e(args, W, world, rank, dev)
+    def stop_timer(self):
+        """Device time of the timed steps on this rank (ms), taken after a synchronize."""
+        self.t_end.record(self.stream)
+        self.torch.cuda.synchronize()
+        self.clocks = self.clk.stop()
+        return self.t_start.elapsed_time(self.t_end)
 
-    if rank == 0:
+    def decode_ms(self, i):
+        return statistics.mean(a.elapsed_time(b) for a, b in self.W[i]["ev"])
+
+    def payload_bits(self, i):
+        return payload_bits(self.W[i]["w"])
+
+    def extras(self, c, ms_total, per_wl):
+        """roofline, e2e, cpu_baseline: the GPU-specific parts of the line."""
+        torch, args, world, rank = self.torch, self.args, self.world, self.rank
+        W = self.W
+        peak, peak_kind = peaks()
+        for i, s in enumerate(W):
+            code = s["code"]
+            # this rank's algorithmic bytes (SURVEY §8(d)): per frame-iteration 2|E| (every int8
+            # message read and rewritten once), per frame once n + ceil(m/8) + ceil(n/8) + 5.
+            frames_g, iters_g = int(c[i, 0]), int(c[i, 4])
+            frac = s["F"] / max(1, frames_g)
+            b_it = 2 * code.n_edges
+            once = code.n + code.mb8 + code.nb8 + 5
+            bytes_rank = frac * (iters_g * b_it + frames_g * once)
+            t = per_wl[s["name"]]["decode_ms"]
+            per_wl[s["name"]].update(alg_bytes=bytes_rank, alg_GBps=bytes_rank / (t / 1000) / 1e9, launch=s["info"])
+        dom = max(per_wl, key=lambda k: per_wl[k]["decode_ms"])
+        achieved = per_wl[dom]["alg_GBps"]
+        traffic, ncu = None, None
+        clocks = self.clocks
+        try:   # from the committed ncu capture of this launch (profiles/traffic.json)
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tj = json.load(f)
+            if tj.get("workload", "C5a") != dom:   # the capture is of another workload's launch
+                raise LookupError
+            traffic = tj.get("decode_dram_bytes_per_launch")
+            ncu = dict(tj.get("ncu") or {}, source=tj.get("source"))
+            if world > 1:   # the capture is of the 1-GPU launch (all frames of the workload)
+                traffic = None
+            elif ncu.get("warp_instructions") and clocks and clocks.get("sm_mhz"):
+                # SURVEY §8(d) co-bound: integer-issue fraction inst_executed / (SMs * 4 * clk * t), with the
+                # captured launch's instruction count (deterministic for this workload) and the live time/clock
+                sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+                ncu["int_issue_frac_live"] = ncu["warp_instructions"] / (
+                    sms * 4 * clocks["sm_mhz"] * 1e6 * per_wl[dom]["decode_ms"] / 1000)
+        except Exception:
+            pass
+        sec_per_step = ms_total / 1000.0 / args.steps
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "ncu": ncu,
+                    "kernel": f"decode_kernel ({dom} launch: {per_wl[dom]['decode_ms']:.1f} ms of "
+                              f"{1000 * sec_per_step:.1f} ms per step)",
+                    "algorithmic_bytes_per_launch": per_wl[dom]["alg_bytes"],
+                    "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}
+        e2e = run_e2e(args, W, world, rank, self.dev)   # end to end through the C ABI, host buffers
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            names = [s["name"] for s in W]
             cores = host_cores()
             per = default_sample(names, cores)
             t0 = time.perf_counter()
@@ -387,25 +408,98 @@ def run_gpu(args):
             sm1 = oracle_sample(names, per1, 1)
             cpu["single_thread_value"], _ = extrapolate(names, sm1, {n: synth.workload(n).frames for n in names})
             cpu["single_thread_sample"] = ", ".join(f"first {per1[n]} frames of {n}" for n in names)
+        return {"roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "dtype": "int8",
+                "paper_context": PAPER_CONTEXT}
+
+
+def load_engine(spec):
+    """--engine module:Class (default: the native engine); the tests plug in a CPU stub."""
+    if not spec:
+        return NativeEngine
+    import importlib
+
+    mod, cls = spec.split(":")
+    return getattr(importlib.import_module(mod), cls)
+
+
+def run_ranks(args, engine_cls):
+    """One process per GPU (rank): prepare this rank's shards, W untimed steps, a barrier, K timed
+    steps, a barrier; time = MAX over ranks; counters = SUM over ranks (the path's one collective).
+    Rank 0 prints the JSON line."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a wrong n_gpus")
+        return 2
+    eng = engine_cls(args, world, rank, local)
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        kw = {"device_id": eng.device_id} if getattr(eng, "device_id", None) is not None else {}
+        dist.init_process_group(eng.backend, **kw)
+    names = eng.prepare()
+    counters = eng.zeros((len(names), 5))
+    for _ in range(args.warmup):
+        eng.step(counters, False)
+        reduce_counters(counters, world)
+    eng.sync()
+    eng.clear_records()
+    if world > 1:
+        dist.barrier()
+    eng.sync()
+    eng.start_timer()
+    for _ in range(args.steps):
+        eng.step(counters, True)
+        reduce_counters(counters, world)                              # a9: the only collective
+    ms_local = eng.stop_timer()
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([ms_local], dtype=torch.float64, device=counters.device)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_total = float(ms.item())
+    c = counters.cpu().numpy()      # last step (identical every step)
+
+    # ---- metric: corrected = syndrome matched and no payload bit error
+    corrected_bits = sum(int(c[i, 1] - c[i, 3]) * eng.payload_bits(i) for i in range(len(names)))
+    processed_bits = sum(int(c[i, 0]) * eng.payload_bits(i) for i in range(len(names)))
+    sec_per_step = ms_total / 1000.0 / args.steps
+    value = corrected_bits / sec_per_step / 1e6
+    processed = processed_bits / sec_per_step / 1e6
+    per_wl = {}
+    for i, name in enumerate(names):
+        frames_g = int(c[i, 0])
+        d = {"decode_ms": eng.decode_ms(i), "frames": frames_g, "fer": 1 - c[i, 1] / max(1, frames_g),
+             "mean_iters": c[i, 4] / max(1, frames_g), "undetected": int(c[i, 3]),
+             "frames_with_errors": int(c[i, 2]),
+             "corrected_key_mbps": int(c[i, 1] - c[i, 3]) * eng.payload_bits(i) / sec_per_step / 1e6,
+             "processed_key_mbps": frames_g * eng.payload_bits(i) / sec_per_step / 1e6}
+        try:
+            d["efficiency_f"] = workload_efficiency(name)
+        except Exception:
+            pass
+        per_wl[name] = d
+    extra = eng.extras(c, ms_total, per_wl)
+    if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-                "scaling": args.scaling, "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-                "config": dict(workload_config(args.workload), parallelism=f"frames sharded over {world} rank(s)",
-                               frames_total={s["name"]: int(c[i, 0]) for i, s in enumerate(W)},
-                               processed_key_mbps=processed, per_workload=per_wl),
-                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": traffic, "ncu": ncu,
-                             "kernel": f"decode_kernel ({dom} launch: {per_wl[dom]['decode_ms']:.1f} ms of "
-                                       f"{1000 * sec_per_step:.1f} ms per step)",
-                             "algorithmic_bytes_per_launch": per_wl[dom]["alg_bytes"],
-                             "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"},
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 4 * len(W) * args.steps,
-                "paper_context": PAPER_CONTEXT,
-                "clocks": clocks}
+                "scaling": args.scaling, "vs_baseline": None, "dtype": extra.pop("dtype", "int8"),
+                "data": "synthetic", "config": workload_config(args.workload, args.gpus, args.scaling),
+                "processed_key_mbps": processed,
+                "frames_total": {name: int(c[i, 0]) for i, name in enumerate(names)},
+                "per_workload": per_wl,
+                "gpu_launches": eng.launches_per_step * args.steps}
+        line.update(extra)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_gpu(args):
+    return run_ranks(args, load_engine(args.engine))
 
 
 def run_e2e(args, W, world, rank, dev):
@@ -471,13 +565,31 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong (default, BASELINE configs[4]: 65536 frames per workload in total, split "
                          "across ranks) or weak (65536 frames per workload on every rank)")
+    ap.add_argument("--engine", default="", help=argparse.SUPPRESS)   # module:Class (tests' CPU stub)
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)
+
+
+def relaunch(n):
+    """`bench.py --gpus N` without a launcher: re-run this command as N ranks (one process per GPU)
+    under torch.distributed.run on this node; rank 0's line is the output."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("bench.py: launching " + " ".join(cmd[1:]))
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":
