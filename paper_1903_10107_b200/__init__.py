@@ -298,20 +298,36 @@ class QCCode:
         Returns (bits, iters, success) host arrays."""
         torch = _torch()
 
-        def hp(a):
+        def hp(a, dtype, shape, name):
+            """Host pointer of a C-contiguous CPU array/tensor of exactly dtype and shape (the library
+            copies F rows of fixed size from/to it, so anything else would be read/written out of bounds)."""
             if a is None:
                 return None
             if isinstance(a, np.ndarray):
-                return ctypes.c_void_p(a.ctypes.data)
-            return ctypes.c_void_p(a.data_ptr())
+                ok = a.dtype == dtype and a.shape == tuple(shape) and a.flags["C_CONTIGUOUS"]
+                got = f"numpy {a.dtype} {a.shape}"
+                ptr = a.ctypes.data
+            else:
+                tdt = {np.uint8: torch.uint8, np.int32: torch.int32}[dtype]
+                ok = (a.device.type == "cpu" and a.dtype == tdt and tuple(a.shape) == tuple(shape)
+                      and a.is_contiguous())
+                got = f"{a.device} {a.dtype} {tuple(a.shape)}"
+                ptr = a.data_ptr()
+            if not ok:
+                raise QkdError(f"{name}: expected a C-contiguous host {np.dtype(dtype).name} array of shape "
+                               f"{tuple(shape)}, got {got}")
+            return ctypes.c_void_p(ptr)
 
-        F = bob_bits.shape[0]
+        F = int(bob_bits.shape[0])
         if out is None:
             out = (np.empty((F, self.nb8), np.uint8), np.empty(F, np.int32), np.empty(F, np.uint8))
         if device_buffer is None:
             device_buffer = torch.empty(self.reconcile_device_bytes(F), dtype=torch.uint8, device="cuda")
-        _check(lib().qkd_reconcile_host(self._h, float(qber), F, hp(bob_bits), hp(known_bits), hp(syndrome),
+        _need(device_buffer, torch.uint8, (device_buffer.numel(),), "device_buffer")
+        args = (hp(bob_bits, np.uint8, (F, self.nb8), "bob_bits"), hp(known_bits, np.uint8, (F, self.nb8), "known_bits"),
+                hp(syndrome, np.uint8, (F, self.mb8), "syndrome"), hp(out[0], np.uint8, (F, self.nb8), "out bits"),
+                hp(out[1], np.int32, (F,), "out iters"), hp(out[2], np.uint8, (F,), "out success"))
+        _check(lib().qkd_reconcile_host(self._h, float(qber), F, args[0], args[1], args[2],
                                         int(max_iter), int(bool(early_stop)), _ptr(device_buffer),
-                                        device_buffer.numel(), hp(out[0]), hp(out[1]), hp(out[2]),
-                                        _stream(stream)))
+                                        device_buffer.numel(), args[3], args[4], args[5], _stream(stream)))
         return out

@@ -7,7 +7,10 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -38,6 +41,34 @@ int fail(int code, const std::string& msg) {
 // --------------------------------------------------------------------------------------
 // code handle
 // --------------------------------------------------------------------------------------
+struct Plan {
+    int variant = 0;   // 1: degree <= 8 smem E, 2: degree <= 20 smem E, 3: generic smem E, 4: generic global E
+    bool pow2 = false; // Z a power of two (byte-OR circulant addressing)
+    int TG = 0, GPC = 0, grid = 0, smem = 0, slot_bytes = 0, e_bytes = 0, tab_off = 0;
+    long long ngroups = 0, slots = 0;
+    size_t ws_L = 0, ws_E = 0, ws_total = 0;
+};
+// qkd_reconcile_host's copy streams and events (up to 8 chunks), kept in the handle and reused
+struct ReconcileCtx {
+    static constexpr int kMaxChunks = 8;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t entry = nullptr;
+    cudaEvent_t ev[2 * kMaxChunks] = {};
+    bool ok = false;
+    ReconcileCtx() {
+        ok = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&entry, cudaEventDisableTiming) == cudaSuccess;
+        for (auto& e : ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    }
+    ~ReconcileCtx() {
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+        if (entry) cudaEventDestroy(entry);
+        if (s_in) cudaStreamDestroy(s_in);
+        if (s_out) cudaStreamDestroy(s_out);
+    }
+};
+
 struct qkd_code {
     int32_t Mb = 0, Nb = 0, Z = 0;
     int64_t n = 0, m = 0, n_edges = 0;
@@ -57,6 +88,11 @@ struct qkd_code {
     std::vector<int> soff;
     int nsplit = 0;
     int* d_soff = nullptr;
+    // host-side caches (the handle is shared between threads): launch plans per (device, F,
+    // QKD_TG_MAX) and the streams/events of qkd_reconcile_host, one context per concurrent call
+    std::mutex mu;
+    std::map<std::tuple<int, long long, int>, Plan> plans;
+    std::vector<ReconcileCtx*> ctx_free;
 };
 
 // --------------------------------------------------------------------------------------
@@ -317,13 +353,7 @@ __global__ void build_llr_float_kernel(int n, int nb8, long long F, float Lc, co
 // --------------------------------------------------------------------------------------
 // launch planning
 // --------------------------------------------------------------------------------------
-struct Plan {
-    int variant = 0;   // 1: degree <= 8 smem E, 2: degree <= 20 smem E, 3: generic smem E, 4: generic global E
-    bool pow2 = false; // Z a power of two (byte-OR circulant addressing)
-    int TG = 0, GPC = 0, grid = 0, smem = 0, slot_bytes = 0, e_bytes = 0, tab_off = 0;
-    long long ngroups = 0, slots = 0;
-    size_t ws_L = 0, ws_E = 0, ws_total = 0;
-};
+
 
 struct DevInfo {
     int sms = 0, smem_optin = 0;
@@ -393,7 +423,45 @@ int choose_variant(int Mb, int64_t n, int64_t m, int nbase, int maxdeg, int smem
     return fits ? 3 : 4;
 }
 
-int make_plan(const qkd_code* c, long long F, Plan& pl) {
+// the kernel's dynamic shared-memory limit, raised once per (kernel, device) to the device maximum
+// (a per-call setting to the plan's size could lower it under another thread's launch)
+int prepare_kernel(const void* k, int dev, int smem_optin) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({k, dev})) return QKD_OK;
+    QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+    done.insert({k, dev});
+    return QKD_OK;
+}
+
+int make_plan_uncached(const qkd_code* c, long long F, Plan& pl);
+
+// launch plan of (code, F) on the current device, cached in the handle: no attribute calls or
+// occupancy queries on the per-call path once a batch size has been seen
+int make_plan(const qkd_code* c_, long long F, Plan& pl) {
+    qkd_code* c = const_cast<qkd_code*>(c_);
+    int dev = 0;
+    QKD_CK(cudaGetDevice(&dev));
+    const char* e = std::getenv("QKD_TG_MAX");
+    const auto key = std::make_tuple(dev, F, e ? atoi(e) : 0);
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        auto it = c->plans.find(key);
+        if (it != c->plans.end()) {
+            pl = it->second;
+            return QKD_OK;
+        }
+    }
+    const int rc = make_plan_uncached(c, F, pl);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->plans.size() >= 256) c->plans.clear();
+    c->plans[key] = pl;
+    return QKD_OK;
+}
+
+int make_plan_uncached(const qkd_code* c, long long F, Plan& pl) {
     int dev = 0;
     QKD_CK(cudaGetDevice(&dev));
     DevInfo di = dev_info(dev);
@@ -432,9 +500,8 @@ int make_plan(const qkd_code* c, long long F, Plan& pl) {
     pl.tab_off = gpc * pl.slot_bytes;
     pl.smem = pl.tab_off + (int)(fixed_tab + gpc * per_slot_tab);
     const void* k = kernel_of(pl.variant, pl.pow2);
-    QKD_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
-    QKD_CK(cudaFuncSetAttribute(kernel_of(pl.variant, pl.pow2, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                pl.smem));
+    if (int rc = prepare_kernel(k, dev, di.smem_optin)) return rc;
+    if (int rc = prepare_kernel(kernel_of(pl.variant, pl.pow2, true), dev, di.smem_optin)) return rc;
     int per_sm = 0;
     QKD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, pl.TG * pl.GPC, pl.smem));
     if (per_sm < 1) return fail(QKD_EUNSUP, "decode kernel cannot be resident with this geometry");
@@ -569,6 +636,7 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
 
 void qkd_code_destroy(qkd_code* c) {
     if (!c) return;
+    for (ReconcileCtx* x : c->ctx_free) delete x;
     if (c->d_layer) cudaFree(c->d_layer);
     if (c->d_edge) cudaFree(c->d_edge);
     if (c->d_kind) cudaFree(c->d_kind);
@@ -775,49 +843,63 @@ int qkd_reconcile_host(const qkd_code* c, double qber, int64_t F, const uint8_t*
     int rc = make_plan(c, F, pl);
     if (rc) return rc;
     const long long per_wave = std::max<long long>(1, pl.slots) * kFramesPerGroup;
-    const int K = (int)std::max<long long>(1, std::min<long long>(8, F / (16 * per_wave)));
-    cudaStream_t s_in = nullptr, s_out = nullptr;
-    std::vector<cudaEvent_t> ev(2 * (size_t)K, nullptr);
-    auto cleanup = [&]() {
-        for (auto& e : ev) if (e) cudaEventDestroy(e);
-        if (s_in) cudaStreamDestroy(s_in);
-        if (s_out) cudaStreamDestroy(s_out);
+    const int K = (int)std::max<long long>(1, std::min<long long>(ReconcileCtx::kMaxChunks, F / (16 * per_wave)));
+    qkd_code* cm = const_cast<qkd_code*>(c);
+    ReconcileCtx* x = nullptr;   // a context of this handle not used by a concurrent call
+    {
+        std::lock_guard<std::mutex> lk(cm->mu);
+        if (!cm->ctx_free.empty()) {
+            x = cm->ctx_free.back();
+            cm->ctx_free.pop_back();
+        }
+    }
+    if (!x) {
+        x = new ReconcileCtx();
+        if (!x->ok) {
+            delete x;
+            return fail(QKD_ECUDA, "cannot create the reconcile streams/events");
+        }
+    }
+    auto release = [&]() {
+        std::lock_guard<std::mutex> lk(cm->mu);
+        cm->ctx_free.push_back(x);
     };
     auto ck = [&](cudaError_t e, const char* what) -> int {
         if (e == cudaSuccess) return QKD_OK;
-        cleanup();
+        release();
         return fail(QKD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
     };
-    if ((rc = ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream"))) return rc;
-    if ((rc = ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream"))) return rc;
-    for (auto& e : ev)
-        if ((rc = ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"))) return rc;
+    // the copies into dbuf must not overtake work already queued on the caller's stream (it may
+    // still be reading a previous use of this buffer): s_in starts behind it
+    if ((rc = ck(cudaEventRecord(x->entry, st), "event"))) return rc;
+    if ((rc = ck(cudaStreamWaitEvent(x->s_in, x->entry, 0), "wait"))) return rc;
+    if ((rc = ck(cudaStreamWaitEvent(x->s_out, x->entry, 0), "wait"))) return rc;
     for (int k = 0; k < K; ++k) {   // all host->device copies, in chunk order
         const long long a = F * k / K, n_k = F * (k + 1) / K - a;
-        if ((rc = ck(cudaMemcpyAsync(d_y + a * nb8, y_h + a * nb8, n_k * nb8, cudaMemcpyHostToDevice, s_in), "h2d"))) return rc;
-        if (d_k && (rc = ck(cudaMemcpyAsync(d_k + a * nb8, known_h + a * nb8, n_k * nb8, cudaMemcpyHostToDevice, s_in), "h2d")))
+        if ((rc = ck(cudaMemcpyAsync(d_y + a * nb8, y_h + a * nb8, n_k * nb8, cudaMemcpyHostToDevice, x->s_in), "h2d"))) return rc;
+        if (d_k && (rc = ck(cudaMemcpyAsync(d_k + a * nb8, known_h + a * nb8, n_k * nb8, cudaMemcpyHostToDevice, x->s_in), "h2d")))
             return rc;
-        if ((rc = ck(cudaMemcpyAsync(d_s + a * mb8, syn_h + a * mb8, n_k * mb8, cudaMemcpyHostToDevice, s_in), "h2d"))) return rc;
-        if ((rc = ck(cudaEventRecord(ev[2 * k], s_in), "event"))) return rc;
+        if ((rc = ck(cudaMemcpyAsync(d_s + a * mb8, syn_h + a * mb8, n_k * mb8, cudaMemcpyHostToDevice, x->s_in), "h2d"))) return rc;
+        if ((rc = ck(cudaEventRecord(x->ev[2 * k], x->s_in), "event"))) return rc;
     }
     for (int k = 0; k < K; ++k) {
         const long long a = F * k / K, n_k = F * (k + 1) / K - a;
-        if ((rc = ck(cudaStreamWaitEvent(st, ev[2 * k], 0), "wait"))) return rc;
+        if ((rc = ck(cudaStreamWaitEvent(st, x->ev[2 * k], 0), "wait"))) return rc;
         rc = qkd_build_llr(c, qber, n_k, d_y + a * nb8, d_k ? d_k + a * nb8 : nullptr, d_llr + a * (long long)c->n, stream);
         if (!rc)
             rc = qkd_decode_batch(c, n_k, d_llr + a * (long long)c->n, d_s + a * mb8, max_iter, early_stop, w, wsb,
                                   d_b + a * nb8, d_it + a, d_su + a, nullptr, nullptr, nullptr, stream);
-        if (rc) { cleanup(); return rc; }
-        if ((rc = ck(cudaEventRecord(ev[2 * k + 1], st), "event"))) return rc;
-        if ((rc = ck(cudaStreamWaitEvent(s_out, ev[2 * k + 1], 0), "wait"))) return rc;
-        if ((rc = ck(cudaMemcpyAsync(bits_h + a * nb8, d_b + a * nb8, n_k * nb8, cudaMemcpyDeviceToHost, s_out), "d2h")))
+        if (rc) { release(); return rc; }
+        if ((rc = ck(cudaEventRecord(x->ev[2 * k + 1], st), "event"))) return rc;
+        if ((rc = ck(cudaStreamWaitEvent(x->s_out, x->ev[2 * k + 1], 0), "wait"))) return rc;
+        if ((rc = ck(cudaMemcpyAsync(bits_h + a * nb8, d_b + a * nb8, n_k * nb8, cudaMemcpyDeviceToHost, x->s_out), "d2h")))
             return rc;
-        if ((rc = ck(cudaMemcpyAsync(iters_h + a, d_it + a, n_k * 4, cudaMemcpyDeviceToHost, s_out), "d2h"))) return rc;
-        if ((rc = ck(cudaMemcpyAsync(succ_h + a, d_su + a, n_k, cudaMemcpyDeviceToHost, s_out), "d2h"))) return rc;
+        if ((rc = ck(cudaMemcpyAsync(iters_h + a, d_it + a, n_k * 4, cudaMemcpyDeviceToHost, x->s_out), "d2h"))) return rc;
+        if ((rc = ck(cudaMemcpyAsync(succ_h + a, d_su + a, n_k, cudaMemcpyDeviceToHost, x->s_out), "d2h"))) return rc;
     }
-    if ((rc = ck(cudaStreamSynchronize(s_out), "sync"))) return rc;
+    if ((rc = ck(cudaStreamSynchronize(x->s_out), "sync"))) return rc;
     if ((rc = ck(cudaStreamSynchronize(st), "sync"))) return rc;
-    cleanup();
+    release();
     return QKD_OK;
 }
 

@@ -1,13 +1,18 @@
 """GPU parity of the exact floating-point BP decoder (fp32, qkd_decode_float_batch) with the fp64
 oracle (R26).
 
-Tolerance (derived, R26): each fp32 box-plus has an absolute error <= ~5e-7 (min exact,
-two log1pf(expf(.)) terms <= ln 2 with <= 2 ulp each); a check-node output passes through <= 2(D-1)
-box-plus evaluations, each 1-Lipschitz in its inputs, and an a-posteriori LLR sums <= 6 messages, so
-after T sweeps |fp32 - fp64| stays below ~ T * 6 * 2D * 5e-7 * (growth) -- the tests use
-atol = 2e-3 * T plus rtol = 1e-5 for large magnitudes.  Decisions (E < 0) and iteration counts of
-full decodes are taken in fp32 on one side and fp64 on the other, so they are compared as
-"identical except where the fp64 margin is within the tolerance"."""
+Tolerance: every fp32 box-plus / sum carries a relative error of a few ulps (2^-24 ~ 6e-8) of its
+magnitude, and the layered sweeps compound it roughly linearly in the sweep count T (each message is
+a 1-Lipschitz function of its inputs).  Measured on B200 (scratch float_err runs, C1/C2/C3, T = 1..12):
+max |fp32 - fp64| / max(1, |fp64|) = 1.1e-6 (T=1), 1.9e-6 (T=2), 4.6e-6 (T=3), 6.8e-6 (T=5), 1.3e-5
+(T=12); large converged LLRs (|E| ~ 1e4) carry proportionally larger absolute errors.  The tests
+use |fp32 - fp64| <= REL * T * max(1, |fp64|) with REL = 4e-6 (2-4x the measured worst case).
+
+Full decodes: a frame's decisions can differ only if some a-posteriori value of its fp64 trajectory
+comes within the tolerance of zero (a decision E < 0, or through it the syndrome test, flips).  So
+every frame must match exactly (bits, iterations, success), EXCEPT frames whose fp64 trajectory has
+min_j |E_j| <= MARGIN * t after some sweep t before both runs stopped -- those are checked only for
+validity (success => syndrome match).  MARGIN = 1e-4 is 25x REL."""
 import numpy as np
 import pytest
 
@@ -15,6 +20,30 @@ import oracle
 import synth
 
 pytestmark = pytest.mark.gpu
+
+REL = 4e-6      # per sweep, relative to max(1, |v|)
+MARGIN = 1e-4   # per sweep: decisions closer to zero than this may legitimately differ
+
+
+def _close(g, o, T, scale=1.0):
+    tol = REL * scale * T * np.maximum(1.0, np.abs(o))
+    return np.abs(g - o) <= tol
+
+
+def _check_full(oc, llr_o, syn, o, g, T, flooding=False):
+    """Frames where fp32 and fp64 disagree must have had a near-zero a-posteriori value on the fp64
+    trajectory (recomputed sweep by sweep with early stop off) before either run stopped."""
+    same = (g["iters"] == o["iters"]) & (g["success"] == o["success"]) & (g["bits"] == o["bits"]).all(axis=1)
+    for f in np.flatnonzero(~same):
+        stop = int(max(g["iters"][f], o["iters"][f]))
+        close = abs(llr_o[f]).min() <= MARGIN
+        for t in range(1, min(stop, T) + 1):
+            r = oracle.decode_float(oc, llr_o[f:f + 1], syn[f:f + 1], t, 0, flooding=flooding)
+            close = close or np.abs(r["E"]).min() <= MARGIN * t
+        assert close, f"frame {f}: fp32 and fp64 differ with every fp64 decision margin above {MARGIN} x sweep"
+    ok = g["success"] == 1
+    assert np.array_equal(oc.syndrome(g["bits"][ok]), syn[ok])       # success => syndrome match
+    return same.mean()
 
 
 def _inputs(name, F):
@@ -39,7 +68,7 @@ def test_float_llr_and_few_sweeps(gpu, name, F):
         g = code.decode_float(llr_g, torch.from_numpy(syn).cuda(), T, False, want_state=True)
         for k in ("E", "L"):
             gv = g[k].cpu().numpy()
-            assert np.allclose(gv, o[k], rtol=1e-5, atol=2e-3 * T), (k, T, np.abs(gv - o[k]).max())
+            assert _close(gv, o[k], T).all(), (k, T, np.abs(gv - o[k]).max())
 
 
 @pytest.mark.parametrize("name,F", [("C1", 64), ("C2", 48)])
@@ -53,10 +82,7 @@ def test_float_full_decodes(gpu, name, F):
     g = code.decode_float(code.build_llr_float(w.qber, torch.from_numpy(y).cuda()), torch.from_numpy(syn).cuda(),
                           w.max_iter, True)
     g = {k: v.cpu().numpy() for k, v in g.items()}
-    same = (g["iters"] == o["iters"]) & (g["success"] == o["success"]) & (g["bits"] == o["bits"]).all(axis=1)
-    assert same.mean() >= 0.95, same.mean()
-    ok = (g["success"] == 1)
-    assert np.array_equal(oc.syndrome(g["bits"][ok]), syn[ok])       # success => syndrome match
+    _check_full(oc, llr_o, syn, o, g, w.max_iter)
 
 
 def test_float_zero_error_frames(gpu):
@@ -83,20 +109,20 @@ def test_flooding_few_sweeps(gpu, name, F):
         g = code.decode_float(llr_g, torch.from_numpy(syn).cuda(), T, False, want_state=True, flooding=True)
         for k in ("E", "L"):
             gv = g[k].cpu().numpy()
-            assert np.allclose(gv, o[k], rtol=1e-5, atol=2e-3 * T), (k, T, np.abs(gv - o[k]).max())
+            assert _close(gv, o[k], T).all(), (k, T, np.abs(gv - o[k]).max())
 
 
 def test_flooding_full_decodes(gpu):
     import torch
 
     w, oc, x, y, syn = _inputs("C1", 64)
-    o = oracle.decode_float(oc, oracle.build_llr_float(oc.n, w.qber, y), syn, w.max_iter, 1, flooding=True)
+    llr_o = oracle.build_llr_float(oc.n, w.qber, y)
+    o = oracle.decode_float(oc, llr_o, syn, w.max_iter, 1, flooding=True)
     code = gpu.QCCode(w.shifts(), w.Z)
     g = code.decode_float(code.build_llr_float(w.qber, torch.from_numpy(y).cuda()), torch.from_numpy(syn).cuda(),
                           w.max_iter, True, flooding=True)
     g = {k: v.cpu().numpy() for k, v in g.items()}
-    same = (g["iters"] == o["iters"]) & (g["success"] == o["success"]) & (g["bits"] == o["bits"]).all(axis=1)
-    assert same.mean() >= 0.95, same.mean()
+    _check_full(oc, llr_o, syn, o, g, w.max_iter, flooding=True)
 
 
 @pytest.mark.parametrize("flooding", [False, True])
@@ -118,4 +144,4 @@ def test_float_degree_21_to_32(gpu, flooding):
         g = code.decode_float(llr_g, torch.from_numpy(syn).cuda(), T, False, want_state=True, flooding=flooding)
         for k in ("E", "L"):
             gv = g[k].cpu().numpy()
-            assert np.allclose(gv, o[k], rtol=1e-5, atol=2e-3 * T), (k, T, np.abs(gv - o[k]).max())
+            assert _close(gv, o[k], T).all(), (k, T, np.abs(gv - o[k]).max())
