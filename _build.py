@@ -54,30 +54,40 @@ def cuda_sources() -> list[str]:
     return srcs
 
 
-def build_cuda(force: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
+def build_cuda(force: bool = False, extra: list[str] | None = None, out: str | None = None,
+               only: list[str] | None = None) -> str:
     """Compile every .cu of csrc/ to an object in parallel (the decode kernel variants are spread over
-    several translation units), then link the shared library."""
+    several translation units), then link the shared library.  `only` (A/B builds): compile just these
+    translation units (basenames) with `extra` and link the product build's objects for the rest."""
     srcs = cuda_sources()
     out = out or os.path.join(ROOT, "paper_1903_10107_b200", "libqkdldpc.so")
     if not (force or extra or _stale(out, srcs + [__file__])):
         return out
     cu = [s for s in srcs if s.endswith(".cu")]
-    objdir = os.path.join(os.path.dirname(out), "build_obj")
+    objdir = os.path.join(os.path.dirname(out), "build_obj") if only is None and not extra else out + ".obj"
     os.makedirs(objdir, exist_ok=True)
     common = [NVCC, *(extra or []), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xfatbin", "-compress-all",
               "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
     jobs = []
+    main_objdir = os.path.join(ROOT, "paper_1903_10107_b200", "build_obj")
     for src in cu:
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if only is not None and os.path.basename(src) not in only:
+            jobs.append((src, os.path.join(main_objdir, os.path.basename(obj)), None))
+            continue
         jobs.append((src, obj, subprocess.Popen([*common, "-c", "-o", obj, src], cwd=ROOT,
                                                 stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     logs, failed = [], []
     for src, obj, proc in jobs:
+        if proc is None:
+            continue
         text = proc.communicate()[0]
         logs.append(f"==== {os.path.basename(src)}\n{text}")
         if proc.returncode != 0:
             failed.append(src)
-    with open(os.path.join(ROOT, "paper_1903_10107_b200", "ptxas.log"), "w") as f:
+    log_path = os.path.join(ROOT, "paper_1903_10107_b200", "ptxas.log") if out.endswith(
+        os.path.join("paper_1903_10107_b200", "libqkdldpc.so")) else out + ".ptxas.log"
+    with open(log_path, "w") as f:
         f.write("\n".join(logs))
     if failed:
         sys.stderr.write("\n".join(logs))

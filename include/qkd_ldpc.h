@@ -157,8 +157,9 @@ int qkd_reconcile_host(const qkd_code* code, double qber, int64_t n_frames,
  *   round k: m - (d - s_k) syndrome-and-reveal bits (host side: R20 with p = d - s_k).
  *   bob_bits_dev, alice_bits_dev [F][ceil(n/8)], syndrome_dev [F][ceil(m/8)] are read only.
  *   work_dev: qkd_adaptive_work_bytes(code, F) bytes.  The code handle's own pos_kind is
- *   ignored (the rounds set the pattern).  Synchronises `stream` once per round (the batch
- *   of still-failed frames is compacted on the host).
+ *   ignored (the rounds set the pattern).  Asynchronous: the list of still-failed frames is
+ *   compacted on the device and every round is enqueued on `stream` without a host
+ *   synchronisation (rounds after all frames matched cost a few empty launches).
  * Errors: QKD_EINVAL (d < 0, s0 outside [0, d], delta < 1, max_rounds < 0, NULL), QKD_EDIM
  * (work buffer too small), QKD_ECUDA. */
 size_t qkd_adaptive_work_bytes(const qkd_code* code, int64_t n_frames);

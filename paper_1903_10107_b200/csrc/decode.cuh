@@ -27,6 +27,7 @@ struct DecParams {
     const int8_t* llr;        // [F][n]
     const uint8_t* syn;       // [F][mb8]
     long long F, ngroups;
+    const long long* F_dev;   // device-resident frame count (<= F) read at kernel start, or null
     int T, early_stop, vec_llr;
     int refill;               // per-frame lane refill (early_stop only, not the lane-pair variant)
     uint32_t* Lws;            // [slots][ws_words]

@@ -195,6 +195,10 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Konst K = p.K.in_regs();
+    // frames of this launch: the host count, or a device-resident count (interactive rounds compact
+    // the still-failed frames on the device, qkd_reconcile_adaptive; the grid is planned for p.F)
+    const long long nF = p.F_dev ? *p.F_dev : p.F;
+    const long long ngroups = (nF + kFramesPerGroup - 1) / kFramesPerGroup;
     // tables: layer info, then one edge table per slot with the slot's E base folded in
     int4* s_layer = reinterpret_cast<int4*>(smem + p.tab_off);
     int2* s_edges = reinterpret_cast<int2*>(s_layer + p.Mb);
@@ -267,7 +271,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
                 fid[f] = -1;
                 if (!((mask >> f) & 1u)) continue;
                 const long long v = a + q++;
-                if (v < p.F) { fid[f] = v; got |= 1u << f; }
+                if (v < nF) { fid[f] = v; got |= 1u << f; }
             }
             if (t == 0)
                 for (int f = 0; f < 4; ++f)
@@ -388,9 +392,9 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
         if (t == 0) ctl[0] = atomicAdd(p.work, 1);
         slot_bar(p, bar);
         const long long g = *(volatile int*)&ctl[0];
-        if (g >= p.ngroups) break;
+        if (g >= ngroups) break;
         const long long f0 = g * kFramesPerGroup;
-        const int nl = (int)min((long long)kFramesPerGroup, p.F - f0);
+        const int nl = (int)min((long long)kFramesPerGroup, nF - f0);
         // frames f0 + f, all with the group's sweep count (built at each finalize call, not kept live)
         auto fin = [&](uint32_t mask, int it, uint32_t succ, uint32_t zeroL) {
             long long fr[4];

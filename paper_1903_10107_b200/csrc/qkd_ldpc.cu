@@ -180,8 +180,8 @@ __global__ void syndrome_qc_kernel(const int4* __restrict__ layer, const int2* _
 // --------------------------------------------------------------------------------------
 __global__ void build_llr_kernel(int n, int nb8, long long F, int Lq, const uint8_t* __restrict__ y,
                                  const uint8_t* __restrict__ known, const uint8_t* __restrict__ kind,
-                                 int8_t* __restrict__ llr) {
-    const long long total = F * nb8;
+                                 int8_t* __restrict__ llr, const long long* __restrict__ F_dev = nullptr) {
+    const long long total = (F_dev ? *F_dev : F) * nb8;   // F_dev: device-resident count (adaptive rounds)
     if ((n & 7) == 0 && (reinterpret_cast<uintptr_t>(llr) & 7) == 0) {
         // one input byte -> one 8-byte store: bit s of y selects -Lq / +Lq for position 8b + s
         const uint32_t pos = (uint32_t)(Lq & 0xFF) * 0x01010101u, neg = (uint32_t)(-Lq & 0xFF) * 0x01010101u;
@@ -296,9 +296,19 @@ __global__ void reveal_kind_kernel(const int32_t* __restrict__ order, long long 
     }
 }
 
-// dst row a = src row idx[a] (row_bytes each); one CTA per row, 4-byte moves when aligned
-__global__ void gather_rows_kernel(const int32_t* __restrict__ idx, long long rows, const uint8_t* __restrict__ src,
-                                   int row_bytes, uint8_t* __restrict__ dst) {
+// The active-frame list of the interactive rounds lives on the device: idx[0..*cnt) are the frame ids
+// still failing, in increasing order; every kernel of a round reads the count from device memory,
+// so the rounds are enqueued back to back without a host synchronisation.
+__global__ void init_active_kernel(int32_t* __restrict__ idx, long long F, long long* __restrict__ cnt) {
+    for (long long a = blockIdx.x * (long long)blockDim.x + threadIdx.x; a < F; a += (long long)gridDim.x * blockDim.x)
+        idx[a] = (int32_t)a;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cnt = F;
+}
+
+// dst row a = src row idx[a] (row_bytes each) for a < *cnt; one CTA per row, 4-byte moves when aligned
+__global__ void gather_rows_kernel(const int32_t* __restrict__ idx, const long long* __restrict__ cnt,
+                                   const uint8_t* __restrict__ src, int row_bytes, uint8_t* __restrict__ dst) {
+    const long long rows = *cnt;
     for (long long a = blockIdx.x; a < rows; a += gridDim.x) {
         const uint8_t* s = src + (long long)idx[a] * row_bytes;
         uint8_t* d = dst + a * row_bytes;
@@ -312,11 +322,12 @@ __global__ void gather_rows_kernel(const int32_t* __restrict__ idx, long long ro
 }
 
 // results of compacted frame a go to frame idx[a] when it matched (or on the last round)
-__global__ void scatter_results_kernel(const int32_t* __restrict__ idx, long long rows, int nb8, int round,
-                                       int last, const uint8_t* __restrict__ cbits, const int32_t* __restrict__ citers,
-                                       const uint8_t* __restrict__ csucc, uint8_t* __restrict__ bits,
-                                       int32_t* __restrict__ iters, int32_t* __restrict__ rounds,
-                                       uint8_t* __restrict__ success) {
+__global__ void scatter_results_kernel(const int32_t* __restrict__ idx, const long long* __restrict__ cnt, int nb8,
+                                       int round, int last, const uint8_t* __restrict__ cbits,
+                                       const int32_t* __restrict__ citers, const uint8_t* __restrict__ csucc,
+                                       uint8_t* __restrict__ bits, int32_t* __restrict__ iters,
+                                       int32_t* __restrict__ rounds, uint8_t* __restrict__ success) {
+    const long long rows = *cnt;
     for (long long a = blockIdx.x; a < rows; a += gridDim.x) {
         if (!csucc[a] && !last) continue;
         const long long f = idx[a];
@@ -327,6 +338,42 @@ __global__ void scatter_results_kernel(const int32_t* __restrict__ idx, long lon
             rounds[f] = round;
         }
     }
+}
+
+// next round's list: the entries of idx_in[0..*cnt_in) whose decode failed, order kept (one CTA of
+// kCompactThreads threads: each takes a contiguous chunk, an exclusive scan of the per-thread counts
+// places the chunks)
+constexpr int kCompactThreads = 1024;
+__global__ void __launch_bounds__(kCompactThreads) compact_failed_kernel(
+        const int32_t* __restrict__ idx_in, const long long* __restrict__ cnt_in, const uint8_t* __restrict__ succ,
+        int32_t* __restrict__ idx_out, long long* __restrict__ cnt_out) {
+    __shared__ long long warp_tot[kCompactThreads / 32];
+    const long long n = *cnt_in;
+    const long long per = (n + kCompactThreads - 1) / kCompactThreads;
+    const long long b = threadIdx.x * per, e = min(n, b + per);
+    long long mine = 0;
+    for (long long a = b; a < e; ++a) mine += succ[a] ? 0 : 1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long incl = mine;                                    // inclusive scan within the warp
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {                                           // scan of the warp totals
+        long long t = lane < kCompactThreads / 32 ? warp_tot[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long v = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += v;
+        }
+        if (lane < kCompactThreads / 32) warp_tot[lane] = t;  // inclusive
+    }
+    __syncthreads();
+    long long out = (wid ? warp_tot[wid - 1] : 0) + incl - mine;
+    for (long long a = b; a < e; ++a)
+        if (!succ[a]) idx_out[out++] = idx_in[a];
+    if (threadIdx.x == kCompactThreads - 1) *cnt_out = out;
 }
 
 
@@ -723,9 +770,11 @@ int qkd_launch_info(const qkd_code* c, int64_t F, int32_t* info) {
     return QKD_OK;
 }
 
-int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint8_t* syn, int32_t max_iter,
-                     int32_t early_stop, void* ws, size_t ws_bytes, uint8_t* bits, int32_t* iters,
-                     uint8_t* success, int8_t* fL, int8_t* fE, int64_t* counters, void* stream) {
+// F_dev (internal, interactive rounds): the launch decodes the first *F_dev <= F frames; the plan
+// (variant, grid, workspace) is the one for F
+static int decode_launch(const qkd_code* c, int64_t F, const long long* F_dev, const int8_t* llr, const uint8_t* syn,
+                         int32_t max_iter, int32_t early_stop, void* ws, size_t ws_bytes, uint8_t* bits,
+                         int32_t* iters, uint8_t* success, int8_t* fL, int8_t* fE, int64_t* counters, void* stream) {
     if (!c || F < 0 || max_iter < 0) return fail(QKD_EINVAL, "bad argument");
     if (F == 0) return QKD_OK;
     if (!llr || !syn || !ws || !bits || !iters || !success) return fail(QKD_EINVAL, "null buffer");
@@ -753,6 +802,7 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
     p.syn = syn;
     p.F = F;
     p.ngroups = pl.ngroups;
+    p.F_dev = F_dev;
     p.T = max_iter;
     p.early_stop = early_stop ? 1 : 0;
     p.vec_llr = (c->n % 4 == 0) && ((reinterpret_cast<uintptr_t>(llr) & 3) == 0);
@@ -784,6 +834,13 @@ int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint
     QKD_CK(cudaLaunchKernel(kernel_of(pl.variant, pl.pow2, p.refill != 0), grid, block, args, pl.smem, st));
     QKD_CK(cudaGetLastError());
     return QKD_OK;
+}
+
+int qkd_decode_batch(const qkd_code* c, int64_t F, const int8_t* llr, const uint8_t* syn, int32_t max_iter,
+                     int32_t early_stop, void* ws, size_t ws_bytes, uint8_t* bits, int32_t* iters,
+                     uint8_t* success, int8_t* fL, int8_t* fE, int64_t* counters, void* stream) {
+    return decode_launch(c, F, nullptr, llr, syn, max_iter, early_stop, ws, ws_bytes, bits, iters, success, fL, fE,
+                         counters, stream);
 }
 
 int qkd_score_batch(const qkd_code* c, int64_t F, const uint8_t* bits, const uint8_t* x, const uint8_t* success,
@@ -908,7 +965,7 @@ size_t qkd_adaptive_work_bytes(const qkd_code* c, int64_t F) {
     const size_t nb8 = (size_t)((c->n + 7) / 8), mb8 = (size_t)((c->m + 7) / 8), Fs = (size_t)std::max<int64_t>(F, 1);
     const size_t ws = qkd_workspace_bytes(c, Fs);
     if (ws == 0) return 0;
-    return align256((size_t)c->n) + align256(Fs * 4) + 3 * align256(Fs * nb8) + align256(Fs * mb8) +
+    return align256((size_t)c->n) + 2 * align256(Fs * 4) + 256 + 3 * align256(Fs * nb8) + align256(Fs * mb8) +
            align256(Fs * (size_t)c->n) + align256(Fs * 4) + align256(Fs) + align256(ws);
 }
 
@@ -928,7 +985,9 @@ int qkd_reconcile_adaptive(const qkd_code* c, double qber, int64_t F, const int3
     const int nb8 = (int)((c->n + 7) / 8), mb8 = (int)((c->m + 7) / 8);
     char* w = static_cast<char*>(work);
     uint8_t* kind = (uint8_t*)w; w += align256((size_t)c->n);
-    int32_t* idx = (int32_t*)w; w += align256((size_t)F * 4);
+    int32_t* idx_a = (int32_t*)w; w += align256((size_t)F * 4);   // active frame ids, double-buffered
+    int32_t* idx_b = (int32_t*)w; w += align256((size_t)F * 4);
+    long long* cnt = (long long*)w; w += 256;                     // cnt[0], cnt[1]: their lengths
     uint8_t* g_bob = (uint8_t*)w; w += align256((size_t)F * nb8);
     uint8_t* g_known = (uint8_t*)w; w += align256((size_t)F * nb8);
     uint8_t* c_bits = (uint8_t*)w; w += align256((size_t)F * nb8);
@@ -938,45 +997,47 @@ int qkd_reconcile_adaptive(const qkd_code* c, double qber, int64_t F, const int3
     uint8_t* c_succ = (uint8_t*)w; w += align256((size_t)F);
     const size_t wsb = qkd_workspace_bytes(c, F);
     cudaStream_t st = (cudaStream_t)stream;
-    std::vector<int32_t> act((size_t)F);
-    for (int64_t f = 0; f < F; ++f) act[(size_t)f] = (int32_t)f;
-    std::vector<uint8_t> ok;
+    // Every round is enqueued without a host synchronisation: the list of still-failed frames and its
+    // length stay on the device (compact_failed_kernel), each kernel reads the length there, and the
+    // decode launch is planned for F and decodes the first *cnt frames.  A round whose list is empty
+    // costs a few empty launches.
+    const int g = (int)std::min<long long>(F, 148LL * 16);
+    init_active_kernel<<<(int)std::min<long long>((F + 255) / 256, 148LL * 8), 256, 0, st>>>(idx_a, F, cnt);
+    QKD_CK(cudaGetLastError());
+    int32_t* cur = idx_a;
+    int32_t* nxt = idx_b;
+    long long* ccur = cnt;
+    long long* cnxt = cnt + 1;
     long long s_prev = -1;
-    for (int k = 0; k <= max_rounds && !act.empty(); ++k) {
+    for (int k = 0; k <= max_rounds; ++k) {
         const long long sk = std::min<long long>(s0 + (long long)k * delta, d);
         if (sk == s_prev) break;                               // nothing left to reveal
         const bool last = (k == max_rounds) || (sk == d);
         s_prev = sk;
-        const long long Fa = (long long)act.size();
         QKD_CK(cudaMemsetAsync(kind, 0, (size_t)c->n, st));
         if (d > 0) {
             reveal_kind_kernel<<<(int)std::min<long long>((d + 255) / 256, 148LL * 8), 256, 0, st>>>(order, d, sk,
                                                                                                    (int)c->n, kind);
             QKD_CK(cudaGetLastError());
         }
-        QKD_CK(cudaMemcpyAsync(idx, act.data(), (size_t)Fa * 4, cudaMemcpyHostToDevice, st));
-        const int g = (int)std::min<long long>(Fa, 148LL * 16);
-        gather_rows_kernel<<<g, 256, 0, st>>>(idx, Fa, bob, nb8, g_bob);
-        gather_rows_kernel<<<g, 256, 0, st>>>(idx, Fa, alice, nb8, g_known);
-        gather_rows_kernel<<<g, 256, 0, st>>>(idx, Fa, syn, mb8, g_syn);
-        const long long total = Fa * nb8;
+        gather_rows_kernel<<<g, 256, 0, st>>>(cur, ccur, bob, nb8, g_bob);
+        gather_rows_kernel<<<g, 256, 0, st>>>(cur, ccur, alice, nb8, g_known);
+        gather_rows_kernel<<<g, 256, 0, st>>>(cur, ccur, syn, mb8, g_syn);
+        const long long total = F * (long long)nb8;
         build_llr_kernel<<<(int)std::min<long long>((total + 255) / 256, 148LL * 64), 256, 0, st>>>(
-            (int)c->n, nb8, Fa, Lq, g_bob, g_known, kind, llr);
+            (int)c->n, nb8, F, Lq, g_bob, g_known, kind, llr, ccur);
         QKD_CK(cudaGetLastError());
-        int rc = qkd_decode_batch(c, Fa, llr, g_syn, max_iter, 1, w, wsb, c_bits, c_iters, c_succ, nullptr, nullptr,
-                                  nullptr, stream);
+        int rc = decode_launch(c, F, ccur, llr, g_syn, max_iter, 1, w, wsb, c_bits, c_iters, c_succ, nullptr,
+                               nullptr, nullptr, stream);
         if (rc) return rc;
-        scatter_results_kernel<<<g, 256, 0, st>>>(idx, Fa, nb8, k, last ? 1 : 0, c_bits, c_iters, c_succ, bits, iters,
-                                                  rounds, success);
+        scatter_results_kernel<<<g, 256, 0, st>>>(cur, ccur, nb8, k, last ? 1 : 0, c_bits, c_iters, c_succ, bits,
+                                                  iters, rounds, success);
         QKD_CK(cudaGetLastError());
-        ok.resize((size_t)Fa);
-        QKD_CK(cudaMemcpyAsync(ok.data(), c_succ, (size_t)Fa, cudaMemcpyDeviceToHost, st));
-        QKD_CK(cudaStreamSynchronize(st));
-        std::vector<int32_t> next;
-        for (long long a = 0; a < Fa; ++a)
-            if (!ok[(size_t)a]) next.push_back(act[(size_t)a]);
         if (last) break;
-        act.swap(next);
+        compact_failed_kernel<<<1, kCompactThreads, 0, st>>>(cur, ccur, c_succ, nxt, cnxt);
+        QKD_CK(cudaGetLastError());
+        std::swap(cur, nxt);
+        std::swap(ccur, cnxt);
     }
     return QKD_OK;
 }

@@ -100,6 +100,12 @@ __device__ __forceinline__ uint32_t tau4(uint32_t a, uint32_t b, const Konst& K)
 // LEA.HI of the flag word (c = (g1 + g2) >> 6), two instructions fewer than tau4.
 //   l <= 2  <=>  g >= 61  (bit 6 of g + 3);   l == 0  <=>  g == 63  (bit 6 of g + 1)
 //   c = [l>=3]([d<2] + [d<6]) + [1<=l<=2][d<4]  as above.
+//
+// Default form (12 SASS: 7 ALU, 5 FMA): the same correction regrouped by the rows of Algorithm 1's
+// table,  c = [l>=1][d<4] + [l>=3][d in {0,1,4,5}]
+//   (l>=3: d<2 -> 1+1, d in 2..3 -> 1+0, d in 4..5 -> 0+1, d>=6 -> 0;  l in 1..2: [d<4];  l = 0: 0)
+// and d in {0,1,4,5} <=> (d & 0x3A) == 0 for d <= 63 (bits 1, 3, 4, 5 clear), so two masked flag
+// words replace three.  Checked against Algorithm 1 over all 64 x 64 inputs on the device (qkd_tau_table).
 __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K) {
     const uint32_t d = __vabsdiffu4(a, b);                       // ALU
 #if QKD_TAU_IMAD
@@ -107,6 +113,16 @@ __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K
 #else
     const uint32_t g = (a + b + d) >> 1;                         // IADD3 + SHF (a+b+d = 2 max <= 126)
 #endif
+#ifndef QKD_TAU14
+    const uint32_t z = imad(g, K.one, 0x01010101u);              // bit6: l == 0
+    const uint32_t p = imad(g, K.one, 0x03030303u);              // bit6: l <= 2
+    const uint32_t W = imad(d, K.one, 0x3C3C3C3Cu);              // bit6: d >= 4
+    const uint32_t Ep = imad(d & 0x3A3A3A3Au, K.one, 0x3F3F3F3Fu);   // bit6: d not in {0,1,4,5}
+    const uint32_t t1 = lop3i<0x02, 0x40404040u>(z, W);          // ~z & ~W & M: l>=1, d<4
+    const uint32_t t2 = lop3i<0x02, 0x40404040u>(p, Ep);         // ~p & ~Ep & M: l>=3, d in {0,1,4,5}
+    const uint32_t y = imad(t1, K.one, t2);                      // 64 c per byte (<= 0x80)
+    return g + (y >> 6);                                         // LEA.HI: 63 - (l - c)
+#else
     const uint32_t p = imad(g, K.one, 0x03030303u);              // bit6: l <= 2
     const uint32_t z = imad(g, K.one, 0x01010101u);              // bit6: l == 0
     const uint32_t U = imad(d, K.one, 0x3E3E3E3Eu);              // bit6: d >= 2
@@ -118,6 +134,7 @@ __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K
     const uint32_t g2 = lop3<0xF8>(t2, p, A);                    // t2 | (p & A)
     const uint32_t y = imad(g1, K.one, g2);                      // 64 c per byte (g1 => g2: <= 0x80)
     return g + (y >> 6);                                         // LEA.HI: 63 - (l - c)
+#endif
 }
 
 // sign-extend bytes {1,3} into 16-bit lanes / zero-extend bytes {1,3}

@@ -104,3 +104,23 @@ def test_adaptive_parity_c4(gpu, q, delta):
                                 torch.from_numpy(x).cuda(), torch.from_numpy(syn).cuda(), w.max_iter)
     g = {k: v.cpu().numpy() for k, v in g.items()}
     assert_same(g, o, keys=("bits", "iters", "success", "rounds"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("F,q_data,rounds", [(2500, 0.07, 7), (300, 0.005, 6), (97, 0.07, 0)])
+def test_adaptive_parity_device_compaction(gpu, F, q_data, rounds):
+    """The round loop keeps the still-failed list on the device (no host sync): many frames (the
+    1024-thread compaction takes chunks of several frames), a batch whose frames all match in round 0
+    (later rounds run on an empty list), and max_rounds = 0 (a single, last round)."""
+    import torch
+
+    shifts, Z, order = _tiny()
+    oc = oracle.Code(shifts, Z)
+    x, y, _ = synth.frames(oc.n, q_data, 777 + F, 0, F)
+    syn = oc.syndrome(x)
+    o = oracle.reveal_rounds(oc, 0.07, y, x, syn, order, 2, 5, rounds, 40)
+    code = gpu.QCCode(shifts, Z)
+    g = code.reconcile_adaptive(0.07, torch.from_numpy(order).cuda(), 2, 5, rounds, torch.from_numpy(y).cuda(),
+                                torch.from_numpy(x).cuda(), torch.from_numpy(syn).cuda(), 40)
+    g = {k: v.cpu().numpy() for k, v in g.items()}
+    assert_same(g, o, keys=("bits", "iters", "success", "rounds"))

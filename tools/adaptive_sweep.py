@@ -7,8 +7,8 @@ For each QBER of BASELINE configs[3] (1, 2, 4, 6, 8 %): frames start at the R19 
 every frame that fails has the next delta = ceil(df (n - d) h2(q)) punctured positions revealed
 (shortened) and is decoded again from scratch, up to --rounds reveals (qkd_reconcile_adaptive).
 Reports per QBER: frame error rate after the rounds, mean efficiency f of the reconciled frames,
-mean reveal rounds, the wall time of the whole interactive reconciliation (CUDA events; the call
-synchronises once per round) and the corrected-key Mbps = reconciled payload bits / time.
+mean reveal rounds, the wall time of the whole interactive reconciliation (CUDA events; since
+round 2 the rounds are enqueued without host synchronisation) and the corrected-key Mbps = reconciled payload bits / time.
 """
 from __future__ import annotations
 
