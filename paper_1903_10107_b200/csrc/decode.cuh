@@ -39,6 +39,8 @@ struct DecParams {
     int8_t* fL;               // [F][n_edges] or null
     int8_t* fE;               // [F][n] or null
     unsigned long long* counters;   // [5] or null
+    unsigned* dbg;            // QKD_RACECHECK builds only: [16] error record, then [slots][n] layer stamps
+    const int* dbg_delta;     // QKD_RACECHECK builds only: per base edge, layers back to the previous writer
     int TG, GPC, slot_bytes, e_bytes, tab_off;
     Konst K;
 };
@@ -192,6 +194,24 @@ __device__ __forceinline__ void ld4_pinned(const uint32_t* p, uint32_t& a, uint3
 __device__ __forceinline__ void st4(uint32_t* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
 __device__ __forceinline__ uint32_t& w4(uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
+// Message loads / stores.  With E in shared memory (ESM) the slot's messages (85 MB for C5a) are
+// re-read from L2 every sweep: plain accesses.  With E in global memory (long frames, variants 7 / 8 /
+// 4) the messages of the resident slots exceed L2 (C4: 148 x 1.3 MB) and would evict the E words
+// every row gathers, so they stream with the evict-first (.cs) policy and E keeps L2.
+#ifndef QKD_MSG_CS
+#define QKD_MSG_CS 1
+#endif
+template <bool ESM>
+__device__ __forceinline__ uint32_t ld_msg(const uint32_t* p) {
+    if constexpr (!ESM && QKD_MSG_CS) return __ldcs(p);
+    else return *p;
+}
+template <bool ESM>
+__device__ __forceinline__ void st_msg(uint32_t* p, uint32_t v) {
+    if constexpr (!ESM && QKD_MSG_CS) __stcs(p, v);
+    else *p = v;
+}
+
 // ---- message layout (every variant but the lane-pair one) -----------------------------------
 // Row r of a block row of degree D keeps its D message words in EMISSION order (word q = the
 // q-th edge row_update emits, emit_pos below), interleaved by 32-row chunks: word q of row r at
@@ -241,7 +261,7 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
     uint32_t P = 0;
     const uint32_t* Lr = msg_row(Lslot, base, D, r);   // word q at Lr[32 q]
 #pragma unroll
-    for (int q = 0; q < D; ++q) S[q] = first ? 0xC0C0C0C0u : Lr[32 * q];
+    for (int q = 0; q < D; ++q) S[q] = first ? 0xC0C0C0C0u : ld_msg<ESM>(Lr + 32 * q);
 #pragma unroll
     for (int k = 0; k < D; ++k) addr[k] = Addr<POW2>::at(et[k], r4, zm4, Z, K);
 #pragma unroll
@@ -279,7 +299,7 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
             tn = edge_out_c(o, sign_s7(Q2, in[k].cw), in[k], ew, K, eo);
         }
         stE<ESM>(Eb, a, eo);
-        Lw[32 * q] = tn;
+        st_msg<ESM>(Lw + 32 * q, tn);
     };
     // magnitudes in complement form (tau4c / edge_magc / edge_out_c): two instructions fewer per tau
 #define QKD_TAU tau4c

@@ -12,6 +12,13 @@
 
 namespace qkd {
 
+// QKD_MUTATE_NOBAR (race-check mutation builds only): drop the barrier between block rows, so the
+// race check must report the resulting stale reads (tools/racecheck.sh)
+#ifdef QKD_MUTATE_NOBAR
+#define QKD_MUTATE_BAR(x)
+#else
+#define QKD_MUTATE_BAR(x) x
+#endif
 
 // the slot's named barrier; with one slot per CTA (e.g. C5a) the id is the immediate 1, so no
 // register holds it across the row updates (it was spilled and reloaded before every barrier)
@@ -22,11 +29,46 @@ __device__ __forceinline__ void slot_bar(const DecParams& p, int bar) {
         group_bar(bar, p.TG);
 }
 
-// One layer (block row) of the slot's rows.
+#ifdef QKD_RACECHECK
+// Layer-order race check (debug builds: tools/racecheck.sh; compute-sanitizer is closed on this GPU
+// pool).  Layers of a slot are numbered lc = 1, 2, ... across sweeps and groups; the row update of
+// layer lc stamps every E word it writes with lc, and before it reads an E word it checks the stamp:
+// the previous writer of that column is the layer delta back (delta = distance to the previous block
+// row holding the same block column, precomputed per base edge), so the stamp must be exactly
+// lc - delta -- smaller means a stale read (the writer's update was not yet visible: a missing or
+// misplaced barrier), larger means a layer ran ahead.  Writers from before the slot's current group
+// (lc - delta < lc0, the group's first layer) are only checked for "not from the future".
+static __device__ __noinline__ void rc_row(const DecParams& p, long long gslot, int4 li, int r, int lc, int lc0, bool write) {
+    unsigned* st = p.dbg + 16 + gslot * (long long)p.n;
+    for (int k = 0; k < li.x; ++k) {
+        const int2 e = p.edge[li.y + k];
+        int idx = r + e.y;
+        idx = idx >= p.Z ? idx - p.Z : idx;
+        const int j = e.x + idx;
+        if (write) {
+            st[j] = (unsigned)lc;
+            continue;
+        }
+        const int want = lc - p.dbg_delta[li.y + k];
+        const int got = (int)st[j];
+        const bool bad = want >= lc0 ? got != want : got >= lc0;
+        if (bad && atomicAdd(p.dbg, 1u) == 0u) {
+            p.dbg[1] = (unsigned)lc; p.dbg[2] = (unsigned)r; p.dbg[3] = (unsigned)(li.y + k);
+            p.dbg[4] = (unsigned)got; p.dbg[5] = (unsigned)want; p.dbg[6] = (unsigned)gslot;
+        }
+    }
+    if (write) __threadfence_block();
+}
+#define QKD_RC(write) rc_row(p, rc_gslot, li, r, rc_lc, rc_lc0, write)
+#else
+#define QKD_RC(write)
+#endif
+
+// One layer (block row) of the slot's rows.  rc_*: layer-order race check (QKD_RACECHECK builds).
 template <int DMAX, bool ESM, bool POW2, bool SPLIT, int FM = 0>
 __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, const int2* et, int t,
                                            unsigned char* Eb, uint32_t* Lslot, const uint8_t* synI, uint32_t fresh,
-                                           const Konst& K) {
+                                           const Konst& K, int rc_lc = 0, int rc_lc0 = 0, long long rc_gslot = 0) {
     const bool first = fresh == 0xFu;   // all four lanes on their first sweep: L = 0 without loading
     const uint32_t zm4 = 4u * (uint32_t)p.Z - 1u;
     if (li.x == 0) return;              // a check row with no variables: nothing to update (oracle: no-op)
@@ -58,9 +100,12 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
 #define QKD_CASE(DD)                                                                                     \
     case DD:                                                                                             \
         if constexpr (DD <= DMAX) {                                                                      \
-            for (int r = t; r < p.Z; r += p.TG)                                                          \
+            for (int r = t; r < p.Z; r += p.TG) {                                                        \
+                QKD_RC(false);                                                                           \
                 row_update<DD, ESM, POW2, (DMAX <= 8 ? 4 : QKD_KEEP_ADDR), FM>(et, p.Z, 4u * r, zm4, Eb, Lslot,   \
                                                                                li.z, r, synI[r], first, K);     \
+                QKD_RC(true);                                                                            \
+            }                                                                                            \
             return;                                                                                      \
         }                                                                                                \
         break;
@@ -75,10 +120,14 @@ __device__ __forceinline__ void layer_pass(const DecParams& p, const int4 li, co
         }
         __trap();   // the host never selects a DMAX kernel for a code with a larger degree
     } else {
-        for (int r = t; r < p.Z; r += p.TG)
+        for (int r = t; r < p.Z; r += p.TG) {
+            QKD_RC(false);
             row_update_generic<ESM>(et, li.x, p.Z, 4u * r, Eb, Lslot, li.z, r, synI[r], first, K);
+            QKD_RC(true);
+        }
     }
 }
+#undef QKD_RC
 
 // per-lane syndrome violation mask (bit f set = frame f violates some parity check),
 // group-uniform, exact for the lanes in `active`.  Hard decision bit = (E < 0) = NOT bit 7 of
@@ -240,6 +289,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
     int* ctl = reinterpret_cast<int*>(sSyn + ((p.m + 15) & ~15));   // [0] group id, [1..2] flags
     uint32_t* flags = reinterpret_cast<uint32_t*>(ctl + 1);
     uint32_t* Lslot = p.Lws + gslot * p.ws_words;
+    int rc_lc = 0, rc_lc0 = 1;   // layer counters of the race check (QKD_RACECHECK builds; otherwise unused)
 
     if constexpr (!SPLIT && REFILL) {
         // ---- per-frame scheduling: a lane whose frame stops is refilled with the next frame at
@@ -370,7 +420,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
             for (int I = 0; I < p.Mb; ++I) {   // idle lanes (no frame left) compute harmlessly
                 const int4 li = s_layer[I];
                 layer_pass<DMAX, ESM, POW2, SPLIT>(p, li, s_edge + li.y, t, Eb, Lslot, sSyn + I * p.Z,
-                                                   fresh == 0xFu ? 0xFu : 0u, K);
+                                                   fresh == 0xFu ? 0xFu : 0u, K, ++rc_lc, rc_lc0, gslot);
                 slot_bar(p, bar);
             }
             ++sweeps;
@@ -393,6 +443,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
         slot_bar(p, bar);
         const long long g = *(volatile int*)&ctl[0];
         if (g >= ngroups) break;
+        rc_lc0 = rc_lc + 1;   // the group's first layer (race check)
         const long long f0 = g * kFramesPerGroup;
         const int nl = (int)min((long long)kFramesPerGroup, nF - f0);
         // frames f0 + f, all with the group's sweep count (built at each finalize call, not kept live)
@@ -466,8 +517,9 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
     for (int I = 0; I < p.Mb; ++I) {                                                                     \
         const int4 li = s_layer[I];                                                                      \
         layer_pass<DMAX, ESM, POW2, SPLIT, FM>(p, li, SPLIT ? s_edge2 + s_soff[I] : s_edge + li.y, t, Eb,   \
-                                               Lslot, sSyn + I * p.Z, FM == 1 ? 0xFu : 0u, K);          \
-        slot_bar(p, bar);                                                                                \
+                                               Lslot, sSyn + I * p.Z, FM == 1 ? 0xFu : 0u, K, ++rc_lc,   \
+                                               rc_lc0, gslot);                                           \
+        QKD_MUTATE_BAR(slot_bar(p, bar));                                                                \
     }
         while (active && it < p.T) {
             ++it;

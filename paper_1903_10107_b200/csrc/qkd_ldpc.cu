@@ -88,6 +88,7 @@ struct qkd_code {
     std::vector<int> soff;
     int nsplit = 0;
     int* d_soff = nullptr;
+    int* d_dbg_delta = nullptr;    // QKD_RACECHECK builds: layers back to each base edge's previous writer
     // host-side caches (the handle is shared between threads): launch plans per (device, F,
     // QKD_TG_MAX) and the streams/events of qkd_reconcile_host, one context per concurrent call
     std::mutex mu;
@@ -648,6 +649,24 @@ int qkd_code_create(const int32_t* base_shifts, int32_t Mb, int32_t Nb, int32_t 
     if (e == cudaSuccess) e = cudaMemcpy(c->d_layer, c->layer.data(), sizeof(int4) * c->layer.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !c->edge.empty())
         e = cudaMemcpy(c->d_edge, c->edge.data(), sizeof(int2) * c->edge.size(), cudaMemcpyHostToDevice);
+#ifdef QKD_RACECHECK
+    if (e == cudaSuccess && !c->edge.empty()) {
+        // delta of base edge (I, J): smallest d in [1, Mb] such that block row (I - d) mod Mb holds J
+        std::vector<int> delta(c->edge.size(), Mb);
+        for (int I = 0; I < Mb; ++I)
+            for (int k = 0; k < c->layer[I].x; ++k) {
+                const int J = c->edge[c->layer[I].y + k].x / Z;
+                for (int d = 1; d <= Mb; ++d) {
+                    const int I2 = ((I - d) % Mb + Mb) % Mb;
+                    bool has = false;
+                    for (int k2 = 0; k2 < c->layer[I2].x; ++k2) has |= c->edge[c->layer[I2].y + k2].x / Z == J;
+                    if (has) { delta[c->layer[I].y + k] = d; break; }
+                }
+            }
+        e = cudaMalloc(&c->d_dbg_delta, sizeof(int) * delta.size());
+        if (e == cudaSuccess) e = cudaMemcpy(c->d_dbg_delta, delta.data(), sizeof(int) * delta.size(), cudaMemcpyHostToDevice);
+    }
+#endif
     if (e == cudaSuccess && c->split) {
         e = cudaMalloc(&c->d_soff, sizeof(int) * c->soff.size());
         if (e == cudaSuccess)
@@ -689,6 +708,7 @@ void qkd_code_destroy(qkd_code* c) {
     if (c->d_kind) cudaFree(c->d_kind);
     if (c->d_payload) cudaFree(c->d_payload);
     if (c->d_soff) cudaFree(c->d_soff);
+    if (c->d_dbg_delta) cudaFree(c->d_dbg_delta);
     delete c;
 }
 
@@ -831,8 +851,29 @@ static int decode_launch(const qkd_code* c, int64_t F, const long long* F_dev, c
     QKD_CK(cudaMemsetAsync(p.work, 0, sizeof(int), st));
     const dim3 grid(pl.grid), block(pl.TG * pl.GPC);
     void* args[] = {&p};
+#ifdef QKD_RACECHECK
+    // debug build: layer stamps per slot, checked by the kernel (decode_kernel.cuh rc_row); the
+    // call synchronises and fails when any E read saw a stale or early stamp
+    const size_t dbg_words = 16 + (size_t)pl.grid * pl.GPC * (size_t)c->n;
+    QKD_CK(cudaMalloc(&p.dbg, dbg_words * 4));
+    QKD_CK(cudaMemsetAsync(p.dbg, 0, dbg_words * 4, st));
+    p.dbg_delta = c->d_dbg_delta;
+#endif
     QKD_CK(cudaLaunchKernel(kernel_of(pl.variant, pl.pow2, p.refill != 0), grid, block, args, pl.smem, st));
     QKD_CK(cudaGetLastError());
+#ifdef QKD_RACECHECK
+    {
+        unsigned rec[8] = {0};
+        QKD_CK(cudaStreamSynchronize(st));
+        QKD_CK(cudaMemcpy(rec, p.dbg, sizeof(rec), cudaMemcpyDeviceToHost));
+        cudaFree(p.dbg);
+        if (rec[0])
+            return fail(QKD_ECUDA, "racecheck: " + std::to_string(rec[0]) + " E reads out of layer order; first: layer " +
+                                       std::to_string(rec[1]) + " row " + std::to_string(rec[2]) + " base edge " +
+                                       std::to_string(rec[3]) + " stamp " + std::to_string((int)rec[4]) + " expected " +
+                                       std::to_string((int)rec[5]) + " slot " + std::to_string(rec[6]));
+    }
+#endif
     return QKD_OK;
 }
 

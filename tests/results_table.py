@@ -1,8 +1,11 @@
 #!/usr/bin/env python
 """BASELINE.md §4 results table: every BASELINE config at its configured batch on one B200.
 
-  python tools/results_table.py [--out gpurun_out/results_table.json] [--reps 5] [--check 64]
+  python tests/results_table.py [--out gpurun_out/results_table.json] [--reps 5] [--check 64]
                                 [--oracle-seconds 3]
+
+Lives under tests/ because it runs the oracle (bit-exactness of spread frames, oracle Mbps): only
+test infrastructure may execute oracle/ (DESIGN §4).
 
 Per workload (C1 64 frames, C2 1024, C3 4096, C4 at each QBER 4096, C5a/C5b 65536):
   * the whole hot path (syndrome a3, LLR a2, decode a4-a8, score a9) timed with CUDA events on the

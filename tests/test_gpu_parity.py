@@ -361,3 +361,20 @@ def test_refill_variant_edge_cases(gpu, monkeypatch, case):
     for T, es in ((9, 1), (1, 0)):
         g, _ = gpu_decode(gpu, shifts, Z, None, llr, syn, T, es)
         assert_same(g, oracle_decode(shifts, Z, llr, syn, T, es))
+
+
+def test_de_profile_code_parity(gpu):
+    """The density-evolution profile of profiles/r2_density_evolution.md (base 16 x 100, Z = 512,
+    n = 51200, rate 0.84; column degrees 2:10, 3:66, 12:24; check degree 31-32, variant 6) built as
+    tools/de_codes.py builds it, on channel frames at QBER 1.8 %, bit-exact against the oracle."""
+    cols = [12] * 24 + [3] * 66 + [2] * 10
+    shifts = synth.girth6_shifts(synth.peg_mask(16, cols, 7), 512, 8)
+    code = gpu.QCCode(shifts, 512)
+    assert code.launch_info(8)["variant"] == 16
+    x, y, _ = synth.frames(100 * 512, 0.018, 203, 0, 6)
+    oc = oracle.Code(shifts, 512)
+    syn = oc.syndrome(x)
+    llr = oc.build_llr(0.018, y)
+    g, _ = gpu_decode(gpu, shifts, 512, None, llr, syn, 50, 1)
+    o = oracle_decode(shifts, 512, llr, syn, 50, 1)
+    assert_same(g, o)

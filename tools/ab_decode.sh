@@ -4,10 +4,10 @@
 wl=$1; F=$2; shift 2
 for rep in 1 2 3; do
   for L in "$@"; do
-    QKD_LIB=$PWD/$L python tools/prof_decode.py --workload $wl --frames $F --reps 5 --check 4 2>&1 | \
+    QKD_LIB=$PWD/$L python tools/prof_decode.py --workload $wl --frames $F --reps 5 2>&1 | \
       python -c "import sys,json
 for l in sys.stdin:
     if l.startswith('{'):
-        d=json.loads(l); print('$L', d['workload'], '%.3f'%d['ms_min'], round(d['alg_GBps']), d.get('oracle_check'))"
+        d=json.loads(l); print('$L', d['workload'], '%.3f'%d['ms_min'], round(d['alg_GBps']))"
   done
 done

@@ -192,6 +192,32 @@ def search(Mb, Nb, degrees, start, iters, budget_s, log):
     return cur, best
 
 
+def _grid_one(args):
+    c, Mb, iters = args
+    return fmt(c), threshold(c, Mb, iters)
+
+
+def grid(Mb, Nb, two, his, nhis, fours, iters, procs, log):
+    """Threshold of every profile {2: n2, 3: rest, 4: n4, hi: n_hi} of the grid (process pool)."""
+    from multiprocessing import Pool
+    jobs = []
+    for n2 in two:
+        for hi in his:
+            for nh in nhis:
+                for n4 in fours:
+                    n3 = Nb - n2 - nh - n4
+                    if n3 < 0:
+                        continue
+                    c = {2: n2, 3: n3, 4: n4, hi: nh}
+                    jobs.append(({k: v for k, v in c.items() if v}, Mb, iters))
+    best = (0.0, None)
+    with Pool(procs) as pool:
+        for key, th in pool.imap_unordered(_grid_one, jobs):
+            log({"counts": key, "threshold": th})
+            best = max(best, (th, key))
+    return best
+
+
 def main():
     ap = argparse.ArgumentParser()
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -207,7 +233,28 @@ def main():
     a2.add_argument("--iters", type=int, default=100)
     a2.add_argument("--budget", type=float, default=1800)
     a2.add_argument("--out", default=None)
+    a3 = sub.add_parser("grid")
+    a3.add_argument("--mb", type=int, default=16)
+    a3.add_argument("--nb", type=int, default=100)
+    a3.add_argument("--two", default="12,14,16,18,20,22,24")
+    a3.add_argument("--hi", default="10,12,14,16")
+    a3.add_argument("--nhi", default="4,6,8,10,12,14,16,18,20")
+    a3.add_argument("--four", default="0")
+    a3.add_argument("--iters", type=int, default=100)
+    a3.add_argument("--procs", type=int, default=os.cpu_count())
+    a3.add_argument("--out", default=None)
     a = ap.parse_args()
+    if a.cmd == "grid":
+        out = open(a.out, "a") if a.out else None
+
+        def glog(d):
+            print(json.dumps(d), flush=True)
+            if out:
+                out.write(json.dumps(d) + "\n"); out.flush()
+        ints = lambda s: [int(x) for x in s.split(",")]   # noqa: E731
+        th, key = grid(a.mb, a.nb, ints(a.two), ints(a.hi), ints(a.nhi), ints(a.four), a.iters, a.procs, glog)
+        glog({"best": key, "threshold": th})
+        return
     if a.cmd == "threshold":
         c = parse_counts(a.counts)
         t0 = time.time()

@@ -1,12 +1,12 @@
 #!/usr/bin/env python
 """Time (and, under ncu, profile) one decode workload in isolation.
 
-  python tools/prof_decode.py [--workload C5a] [--frames 4736] [--reps 5] [--check 8]
+  python tools/prof_decode.py [--workload C5a] [--frames 4736] [--reps 5]
 
 Prints one JSON line per workload: mean/min decode ms over --reps launches (CUDA events on the
 launching stream), algorithmic GB/s (per-frame iterations x 2|E| + once-bytes) and
-the launch plan.  --check K compares the first K frames with the oracle (test infrastructure,
-like bench.py's cpu_baseline leg).  Under ncu use --reps 1.
+the launch plan.  Under ncu use --reps 1.  (Parity of an A/B build: QKD_LIB=<lib> pytest tests -m gpu;
+tools never run the oracle.)
 """
 from __future__ import annotations
 
@@ -31,7 +31,6 @@ def main():
     ap.add_argument("--frames", type=int, default=4736)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--max-iter", type=int, default=None)
-    ap.add_argument("--check", type=int, default=0)
     a = ap.parse_args()
     for name in a.workload.split(","):
         w = synth.workload(name)
@@ -59,14 +58,6 @@ def main():
         out = dict(workload=name, frames=a.frames, T=T, ms_mean=sum(times) / len(times), ms_min=t,
                    alg_GBps=alg / (t * 1e-3) / 1e9, mean_iters=float(iters.mean()),
                    success=float(r["success"].float().mean().item()), launch=code.launch_info(a.frames))
-        if a.check:
-            import oracle
-
-            oc = oracle.Code(w.shifts(), w.Z)
-            k = a.check
-            o = oc.decode(oc.build_llr(w.qber, y[:k], w.pos_kind(), x[:k] if w.pos_kind() is not None else None), oc.syndrome(x[:k]), T, 1, want_state=False)
-            ok = all(np.array_equal(r[f][:k].cpu().numpy(), o[f]) for f in ("bits", "iters", "success"))
-            out["oracle_check"] = f"{k} frames {'bit-exact' if ok else 'MISMATCH'}"
         print(json.dumps(out), flush=True)
 
 
