@@ -54,6 +54,9 @@ constexpr int kFramesPerGroup = 4;   // frames per SWAR word (one byte lane each
 #define QKD_D32_THREADS 512
 #endif
 #define QKD_D32_TG(DMAX) ((DMAX) == 32 ? QKD_D32_THREADS : 512)
+#ifndef QKD_G8_THREADS
+#define QKD_G8_THREADS 1024   // variant 7 (degree <= 8, E in global memory): threads per CTA (C4: 512 -> 1024
+#endif                        // with QKD_G8_LOWREG, 69.2 -> 61.7 ms; 768 threads: 72.2 ms, uneven rows)
 #ifndef QKD_G32_THREADS
 #define QKD_G32_THREADS 256   // variant 8 (degree <= 32, E in global memory): 254 registers, no spills
 #endif
@@ -254,7 +257,11 @@ __device__ __forceinline__ void row_update(const int2* __restrict__ et, int Z, u
 #ifndef QKD_LOWREG_MIN
 #define QKD_LOWREG_MIN 21
 #endif
-    constexpr bool LOWREG = D >= QKD_LOWREG_MIN;
+#ifndef QKD_G8_LOWREG
+#define QKD_G8_LOWREG 1   // variant 7 (E in global memory, degree <= 8) rows keep only cw + old message per edge
+                          // (64 registers at 1024 threads without spills in the row loop)
+#endif
+    constexpr bool LOWREG = D >= QKD_LOWREG_MIN || (!ESM && D <= 8 && QKD_G8_LOWREG);
     uint32_t addr[D];
     EdgeIn in[D];
     uint32_t S[D];                                 // the row's message words, emission order

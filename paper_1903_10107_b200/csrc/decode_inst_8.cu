@@ -9,5 +9,6 @@ template __global__ void decode_kernel<8, true, false, false, false>(const DecPa
 template __global__ void decode_kernel<8, true, true, false, true>(const DecParams);
 template __global__ void decode_kernel<8, true, false, false, true>(const DecParams);
 template __global__ void decode_kernel<8, false, false, false, false>(const DecParams);
+template __global__ void decode_kernel<8, false, true, false, false>(const DecParams);
 
 }  // namespace qkd

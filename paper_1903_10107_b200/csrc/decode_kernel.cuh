@@ -240,7 +240,7 @@ static __device__ void finalize(const DecParams& p, const int4* s_layer, const u
 }
 
 template <int DMAX, bool ESM, bool POW2, bool SPLIT, bool REFILL>
-__global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 32 && !ESM ? QKD_G32_THREADS : (DMAX == 20 || DMAX == 32 || DMAX == 8 ? QKD_D32_TG(DMAX) : 256)), 1)
+__global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 8 && !ESM ? QKD_G8_THREADS : (DMAX == 32 && !ESM ? QKD_G32_THREADS : (DMAX == 20 || DMAX == 32 || DMAX == 8 ? QKD_D32_TG(DMAX) : 256))), 1)
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Konst K = p.K.in_regs();
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 
     for (int i = threadIdx.x; i < p.GPC * p.nbase; i += blockDim.x) {
         const int sl = i / p.nbase;
         const int2 e = p.edge[i - sl * p.nbase];
-        s_edges[i] = POW2 ? make_int2(sl * p.slot_bytes + 4 * e.x, 4 * e.y) : e;
+        s_edges[i] = POW2 ? make_int2((ESM ? sl * p.slot_bytes : 0) + 4 * e.x, 4 * e.y) : e;   // global E: per-slot base pointer
     }
     if constexpr (SPLIT) {
         for (int I = 0; I < p.Mb; ++I) {

@@ -441,7 +441,7 @@ const void* kernel_of(int variant, bool pow2, bool refill = false) {
         case 2: return pow2 ? kfun<20, true, true>() : kfun<20, true, false>();
         case 3: return kfun<0, true, false>();
         case 6: return pow2 ? kfun<32, true, true>() : kfun<32, true, false>();
-        case 7: return kfun<8, false, false>();
+        case 7: return pow2 ? kfun<8, false, true>() : kfun<8, false, false>();
         case 8: return kfun<32, false, false>();
         case 5: return pow2 ? kfun<20, true, true, true>() : kfun<20, true, false, true>();
         default: return kfun<0, false, false>();
@@ -519,9 +519,10 @@ int make_plan_uncached(const qkd_code* c, long long F, Plan& pl) {
     const long long e_bytes = 4LL * c->n;
     pl.variant = choose_variant(c->Mb, c->n, c->m, c->nbase, c->maxdeg, di.smem_optin, c->split);
     if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
-    pl.pow2 = (pl.variant <= 2 || pl.variant == 5 || pl.variant == 6) && ((c->Z & (c->Z - 1)) == 0);   // smem E only
+    // byte-OR addressing: smem E variants, and variant 7 (one slot per CTA, E offsets from the slot's global base)
+    pl.pow2 = (pl.variant <= 2 || pl.variant == 5 || pl.variant == 6 || pl.variant == 7) && ((c->Z & (c->Z - 1)) == 0);
     int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024
-                 : (pl.variant == 2 || pl.variant == 7 ? 512 : (pl.variant == 8 ? QKD_G32_THREADS : (pl.variant == 6 ? QKD_D32_THREADS : 256)));
+                 : (pl.variant == 2 ? 512 : (pl.variant == 7 ? QKD_G8_THREADS : (pl.variant == 8 ? QKD_G32_THREADS : (pl.variant == 6 ? QKD_D32_THREADS : 256))));
     if (const char* e = std::getenv("QKD_TG_MAX"))   // experiments: fewer threads per frame group
         tg_max = std::max(32, std::min(tg_max, atoi(e) / 32 * 32));
     if (pl.variant == 5)   // two lanes per row, 16 rows per warp

@@ -54,7 +54,7 @@ def test_c4_full_batch(gpu, monkeypatch, q, greg):
     llr = oc.build_llr(w.qber, y, kind, x)
     r, code = _run(gpu, shifts, w.Z, kind, x, y, llr, syn, w.max_iter)
     info = code.launch_info(F_FULL)
-    assert info["variant"] == (7 if greg == "1" else 4)
+    assert info["variant"] % 10 == (7 if greg == "1" else 4)
     assert info["groups"] > 2 * info["grid"] * info["groups_per_cta"]     # slots reuse their workspace
     _compare(r, shifts, w.Z, llr, syn, w.max_iter, _sample(F_FULL))
 

@@ -73,7 +73,7 @@ def test_random_long_codes(gpu, seed):
     sh = sh.astype(np.int32)
     llr, syn = _frames(sh, Z, 5000 + seed, F=3)
     g, code = gpu_decode(gpu, sh, Z, None, llr, syn, 6, seed % 2)
-    assert code.launch_info(3)["variant"] in (4, 7, 8)
+    assert code.launch_info(3)["variant"] % 10 in (4, 7, 8)
     o = oracle_decode(sh, Z, llr, syn, 6, seed % 2)
     assert_same(g, o)
 

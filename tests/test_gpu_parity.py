@@ -292,7 +292,7 @@ def test_global_e_variants(gpu, monkeypatch, greg):
         monkeypatch.setenv("QKD_NO_GREG", "1")
     w, shifts, kind, x, y, llr, syn = workload_inputs("C4@0.04", 5)
     g, code = gpu_decode(gpu, shifts, w.Z, kind, llr, syn, 9, 0)
-    assert code.launch_info(5)["variant"] == (7 if greg == "1" else 4)
+    assert code.launch_info(5)["variant"] % 10 == (7 if greg == "1" else 4)
     o = oracle_decode(shifts, w.Z, llr, syn, 9, 0)
     assert_same(g, o)
 
