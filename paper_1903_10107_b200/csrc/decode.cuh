@@ -54,6 +54,9 @@ constexpr int kFramesPerGroup = 4;   // frames per SWAR word (one byte lane each
 #define QKD_D32_THREADS 512
 #endif
 #define QKD_D32_TG(DMAX) ((DMAX) == 32 ? QKD_D32_THREADS : 512)
+#ifndef QKD_V1_THREADS
+#define QKD_V1_THREADS 1024   // variant 1 (degree <= 8, E in shared memory): threads per CTA
+#endif
 #ifndef QKD_G8_THREADS
 #define QKD_G8_THREADS 1024   // variant 7 (degree <= 8, E in global memory): threads per CTA (C4: 512 -> 1024
 #endif                        // with QKD_G8_LOWREG, 69.2 -> 61.7 ms; 768 threads: 72.2 ms, uneven rows)
@@ -68,11 +71,18 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 // E addressing.  POW2: a = ((r4 + s4) & (4Z - 1)) | cb4, all in bytes, cb4 = slot E base + J*Z*4
 // (slot bases are multiples of 4Z, see make_plan), one IMAD + one LOP3 per edge.  Otherwise
 // words: j = J*Z + (r + s) mod Z.
+// experiments (A/B): bit 1 the guard's +1, bit 2 the magnitude's 63 - v, bit 4 the circulant address add
+// as plain adds (ptxas: VIADD / IADD3) instead of IMAD with the opaque multiplier
+#ifndef QKD_VIADD_MISC
+#define QKD_VIADD_MISC 0
+#endif
+#define QKD_MISC_ADD(x, c, BIT) ((QKD_VIADD_MISC & (BIT)) ? (x) + (c) : imad((x), K.one, (c)))
+
 template <bool POW2>
 struct Addr {
     __device__ __forceinline__ static uint32_t at(int2 e, uint32_t r4, uint32_t zm4, int Z, const Konst& K) {
         if constexpr (POW2) {
-            return (imad(r4, K.one, (uint32_t)e.y) & zm4) | (uint32_t)e.x;
+            return (QKD_MISC_ADD(r4, (uint32_t)e.y, 4) & zm4) | (uint32_t)e.x;
         } else {
             int idx = (int)(r4 >> 2) + e.y;
             idx = idx >= Z ? idx - Z : idx;
@@ -119,7 +129,7 @@ __device__ __forceinline__ uint32_t edge_mag(uint32_t cw, const Konst& K) { retu
 
 // complement form 63 - min(|x|, 63) of the same magnitude (input of tau4c)
 __device__ __forceinline__ uint32_t edge_magc(uint32_t cw, const Konst& K) {
-    return imad(__vabsdiffu4(cw, K.c63), K.m1, 0x3F3F3F3Fu);
+    return (QKD_VIADD_MISC & 2) ? 0x3F3F3F3Fu - __vabsdiffu4(cw, K.c63) : imad(__vabsdiffu4(cw, K.c63), K.m1, 0x3F3F3F3Fu);
 }
 
 // The same value by a different instruction sequence (immediate operand, IADD3): ptxas cannot
@@ -141,7 +151,7 @@ __device__ __forceinline__ uint32_t edge_out_s(uint32_t oc, uint32_t s7, uint32_
     const uint32_t hi = imad(hi16z(ew), K.one, hi16z(d));         // lanes {1,3}: ew + d
     const uint32_t lo = imadi<-256>(hi, imad(ew, K.one, d));     // lanes {0,2}
     const uint32_t enew = pack16c(relu_min(lo, K.b128, 0x00FE00FEu), relu_min(hi, K.b128, 0x00FE00FEu), K);
-    const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
+    const uint32_t G = bmask7(QKD_MISC_ADD(__vabsdiffu4(ew, K.c127), 0x01010101u, 1));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);
     return sn;
 }
@@ -158,7 +168,7 @@ __device__ __forceinline__ uint32_t edge_out(uint32_t o, uint32_t s7, const Edge
     const uint32_t tlo = imad(imad(thi, K.m256, Tb), K.one, 0xFFFFFF00u);   // lanes {0,2}, same
     // E + L_new - L_old = x + L_new: lanes relu(min(X + T - 128, 254)) = clamp(.., -127, 127) + 127
     const uint32_t enew = pack16c(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu), K);
-    const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
+    const uint32_t G = bmask7(QKD_MISC_ADD(__vabsdiffu4(ew, K.c127), 0x01010101u, 1));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);                              // G ? ew : enew
     return Tb;                                                    // 192 + L_new (stored as is)
 }
@@ -179,7 +189,7 @@ __device__ __forceinline__ uint32_t edge_out_c(uint32_t oc, uint32_t s7, const E
     const uint32_t tlo = imadi<-256>(thi, imad(Tb, K.one, 0xFFFFFF00u));
 #endif
     const uint32_t enew = pack16c(relu_min(in.xlo, tlo, 0x00FE00FEu), relu_min(in.xhi, thi, 0x00FE00FEu), K);
-    const uint32_t G = bmask7(imad(__vabsdiffu4(ew, K.c127), K.one, 0x01010101u));   // |E| == 127
+    const uint32_t G = bmask7(QKD_MISC_ADD(__vabsdiffu4(ew, K.c127), 0x01010101u, 1));   // |E| == 127
     e_out = lop3<0xCA>(G, ew, enew);
     return Tb;                                                    // 192 + L_new
 }

@@ -240,7 +240,7 @@ static __device__ void finalize(const DecParams& p, const int4* s_layer, const u
 }
 
 template <int DMAX, bool ESM, bool POW2, bool SPLIT, bool REFILL>
-__global__ void __launch_bounds__(SPLIT || (DMAX == 8 && ESM) ? 1024 : (DMAX == 8 && !ESM ? QKD_G8_THREADS : (DMAX == 32 && !ESM ? QKD_G32_THREADS : (DMAX == 20 || DMAX == 32 || DMAX == 8 ? QKD_D32_TG(DMAX) : 256))), 1)
+__global__ void __launch_bounds__(SPLIT ? 1024 : (DMAX == 8 && ESM) ? QKD_V1_THREADS : (DMAX == 8 && !ESM ? QKD_G8_THREADS : (DMAX == 32 && !ESM ? QKD_G32_THREADS : (DMAX == 20 || DMAX == 32 || DMAX == 8 ? QKD_D32_TG(DMAX) : 256))), 1)
     decode_kernel(const DecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Konst K = p.K.in_regs();

@@ -521,7 +521,7 @@ int make_plan_uncached(const qkd_code* c, long long F, Plan& pl) {
     if ((pl.variant == 5) != c->split) return fail(QKD_EUNSUP, "code was created for another device geometry");
     // byte-OR addressing: smem E variants, and variant 7 (one slot per CTA, E offsets from the slot's global base)
     pl.pow2 = (pl.variant <= 2 || pl.variant == 5 || pl.variant == 6 || pl.variant == 7) && ((c->Z & (c->Z - 1)) == 0);
-    int tg_max = (pl.variant == 1 || pl.variant == 5) ? 1024
+    int tg_max = pl.variant == 5 ? 1024 : pl.variant == 1 ? QKD_V1_THREADS
                  : (pl.variant == 2 ? 512 : (pl.variant == 7 ? QKD_G8_THREADS : (pl.variant == 8 ? QKD_G32_THREADS : (pl.variant == 6 ? QKD_D32_THREADS : 256))));
     if (const char* e = std::getenv("QKD_TG_MAX"))   // experiments: fewer threads per frame group
         tg_max = std::max(32, std::min(tg_max, atoi(e) / 32 * 32));

@@ -1,12 +1,13 @@
 // swar.cuh -- packed 4-frame (u8x4) and 2-frame (16x2) integer arithmetic for the sm_100a
 // decode kernels.  Each 32-bit word holds one int8 quantity for 4 independent frames (frame f
 // in byte f).  Only ops that are native on sm_100a are used:
-//   ALU pipe: LOP3, SHF, PRMT, VABSDIFF4.U8, VIMNMX/VIADDMNMX(.RELU).S16x2
-//   FMA pipe: IMAD, VIADD.16x2
-// Both pipes issue one warp instruction every 2 cycles per SM sub-partition (measured with
-// tools/pipe_probe.cu), so the arithmetic below is written to split evenly between them: adds
-// of constants, shifts-left, negations and 16-bit lane unpacking go through IMAD with an opaque
-// runtime multiplier (Konst), which ptxas cannot fold back into an ALU-pipe IADD3.
+//   ALU pipe: LOP3, IADD3 (one warp instruction per cycle per SM sub-partition), SHF, PRMT,
+//             VABSDIFF4.U8, VIMNMX/VIADDMNMX(.RELU).S16x2 (one every 2 cycles)
+//   FMA pipe: IMAD (every operand form), VIADD.16x2 (one every 2 cycles)
+// (tools/pipe_probe*.cu on the B200, profiles/r2_pipe_probe*.txt).  The row update is bound by
+// instruction issue first, then by these pipes: adds of constants, shifts-left, negations
+// and 16-bit lane unpacking go through IMAD with an opaque runtime multiplier (Konst) where that keeps
+// the ALU pipe's half-rate ops from queueing, IADD3 where the ALU pipe has room.
 #pragma once
 #include <cstdint>
 
@@ -114,13 +115,19 @@ __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K
     const uint32_t g = (a + b + d) >> 1;                         // IADD3 + SHF (a+b+d = 2 max <= 126)
 #endif
 #ifndef QKD_TAU14
-    const uint32_t z = imad(g, K.one, 0x01010101u);              // bit6: l == 0
-    const uint32_t p = imad(g, K.one, 0x03030303u);              // bit6: l <= 2
-    const uint32_t W = imad(d, K.one, 0x3C3C3C3Cu);              // bit6: d >= 4
-    const uint32_t Ep = imad(d & 0x3A3A3A3Au, K.one, 0x3F3F3F3Fu);   // bit6: d not in {0,1,4,5}
+#ifndef QKD_TAU_ADDS
+#define QKD_TAU_ADDS 3   // which of the tau's constant adds are plain adds (ptxas: VIADD) instead of IMAD;
+                         // 3 (the four threshold adds) measured 1 % faster on C5a than 0 (all IMAD)
+#endif
+#define QKD_ADD(x, c, BIT) ((QKD_TAU_ADDS & (BIT)) ? (x) + (c) : imad((x), K.one, (c)))
+    const uint32_t z = QKD_ADD(g, 0x01010101u, 1);               // bit6: l == 0
+    const uint32_t p = QKD_ADD(g, 0x03030303u, 1);               // bit6: l <= 2
+    const uint32_t W = QKD_ADD(d, 0x3C3C3C3Cu, 2);               // bit6: d >= 4
+    const uint32_t Ep = QKD_ADD(d & 0x3A3A3A3Au, 0x3F3F3F3Fu, 2);   // bit6: d not in {0,1,4,5}
     const uint32_t t1 = lop3i<0x02, 0x40404040u>(z, W);          // ~z & ~W & M: l>=1, d<4
     const uint32_t t2 = lop3i<0x02, 0x40404040u>(p, Ep);         // ~p & ~Ep & M: l>=3, d in {0,1,4,5}
-    const uint32_t y = imad(t1, K.one, t2);                      // 64 c per byte (<= 0x80)
+    const uint32_t y = QKD_ADD(t1, t2, 4);                       // 64 c per byte (<= 0x80)
+#undef QKD_ADD
     return g + (y >> 6);                                         // LEA.HI: 63 - (l - c)
 #else
     const uint32_t p = imad(g, K.one, 0x03030303u);              // bit6: l <= 2

@@ -9,7 +9,9 @@ Each profile "Mb,Nb,Z;d:count,..." is built as synth.peg_qc_code builds codes (P
 P:155 / Hu et al., then girth >= 6 circulant shifts), seed 7; frames are the seeded BSC frames of
 synth.frames (C3's data seed 203, so the rate-0.84 codes see the same channel draws at every QBER);
 the decoder is the product (T = 50, early stop, int8 LLRs at the frame's QBER).  f = (Mb / Nb) / h(q)
-(R20, no puncturing).  Parity of such codes against the oracle: tests/test_gpu_parity.py.
+(R20, no puncturing).  --float adds exact floating-point BP (N1) on the same frames: the BP
+waterfall of the profile, against which the quantized decoder's loss is read.  Parity of such codes
+against the oracle: tests/test_gpu_parity.py.
 """
 from __future__ import annotations
 
@@ -52,6 +54,7 @@ def main():
     ap.add_argument("--qbers", default="0.015,0.016,0.017,0.018,0.019,0.02,0.021")
     ap.add_argument("--frames", type=int, default=4096)
     ap.add_argument("--T", type=int, default=50)
+    ap.add_argument("--float", action="store_true", help="also exact floating-point BP (N1, qkd_decode_float_batch)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     rows = []
@@ -80,6 +83,14 @@ def main():
                        frames=a.frames, fer=float(1 - ok.mean()), undetected=int((succ & (err > 0)).sum()),
                        mean_iters=float(r["iters"].float().mean().item()), decode_ms=e0.elapsed_time(e1),
                        build_s=round(time.time() - t0, 1))
+            if a.float:
+                lf = code.build_llr_float(q, ys)
+                rf = code.decode_float(lf, syn, a.T, True)
+                torch.cuda.synchronize()
+                ef = code.score(rf["bits"], xs, rf["success"], want_errors=True).cpu().numpy()
+                sf = rf["success"].cpu().numpy() == 1
+                row.update(fer_float=float(1 - (sf & (ef == 0)).mean()),
+                           mean_iters_float=float(rf["iters"].float().mean().item()))
             rows.append(row)
             print(json.dumps(row), flush=True)
     if a.out:
