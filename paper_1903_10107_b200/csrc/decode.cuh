@@ -55,7 +55,9 @@ constexpr int kFramesPerGroup = 4;   // frames per SWAR word (one byte lane each
 #endif
 #define QKD_D32_TG(DMAX) ((DMAX) == 32 ? QKD_D32_THREADS : 512)
 #ifndef QKD_V1_THREADS
-#define QKD_V1_THREADS 1024   // variant 1 (degree <= 8, E in shared memory): threads per CTA
+#define QKD_V1_THREADS 1024   // variant 1 (degree <= 8, E in shared memory): threads per CTA.  768 (80 registers, no
+                              // spill in the refill kernel) speeds C2 at its 1024 frames up 10 % but slows the bench's
+                              // 65536-frame C5b by 3 % (17.6 -> 18.2 ms), so the bench's configuration keeps 1024.
 #endif
 #ifndef QKD_G8_THREADS
 #define QKD_G8_THREADS 1024   // variant 7 (degree <= 8, E in global memory): threads per CTA (C4: 512 -> 1024
