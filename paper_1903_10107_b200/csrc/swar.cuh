@@ -1,8 +1,8 @@
 // swar.cuh -- packed 4-frame (u8x4) and 2-frame (16x2) integer arithmetic for the sm_100a
 // decode kernels.  Each 32-bit word holds one int8 quantity for 4 independent frames (frame f
 // in byte f).  Only ops that are native on sm_100a are used:
-//   ALU pipe: LOP3, IADD3 (one warp instruction per cycle per SM sub-partition), SHF, PRMT,
-//             VABSDIFF4.U8, VIMNMX/VIADDMNMX(.RELU).S16x2 (one every 2 cycles)
+//   ALU pipe: LOP3, IADD3, SHF, PRMT, VABSDIFF4.U8, VIMNMX/VIADDMNMX(.RELU).S16x2 (one warp
+//             instruction every 2 cycles per SM sub-partition)
 //   FMA pipe: IMAD (every operand form), VIADD.16x2 (one every 2 cycles)
 // (tools/pipe_probe*.cu on the B200, profiles/r2_pipe_probe*.txt).  The row update is bound by
 // instruction issue first, then by these pipes: adds of constants, shifts-left, negations
