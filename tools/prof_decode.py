@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--frames", type=int, default=4736)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--max-iter", type=int, default=None)
+    ap.add_argument("--early-stop", type=int, default=1, help="0: no per-iteration syndrome check (all T sweeps)")
     a = ap.parse_args()
     for name in a.workload.split(","):
         w = synth.workload(name)
@@ -46,7 +47,7 @@ def main():
         for _ in range(a.reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            r = code.decode(llr, syn, T, True, workspace=ws)
+            r = code.decode(llr, syn, T, bool(a.early_stop), workspace=ws)
             e1.record(st)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -55,7 +56,7 @@ def main():
         once = code.n + code.mb8 + code.nb8 + 5
         alg = float(iters.sum() * 2 * n_edges + a.frames * once)
         t = min(times)
-        out = dict(workload=name, frames=a.frames, T=T, ms_mean=sum(times) / len(times), ms_min=t,
+        out = dict(workload=name, frames=a.frames, T=T, early_stop=a.early_stop, ms_mean=sum(times) / len(times), ms_min=t,
                    alg_GBps=alg / (t * 1e-3) / 1e9, mean_iters=float(iters.mean()),
                    success=float(r["success"].float().mean().item()), launch=code.launch_info(a.frames))
         print(json.dumps(out), flush=True)
