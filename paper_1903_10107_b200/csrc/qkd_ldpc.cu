@@ -450,7 +450,7 @@ const void* kernel_of(int variant, bool pow2, bool refill = false) {
 
 // 1, 2, -1, -2, -256 as kernel arguments: opaque to ptxas, so a*one + c stays an IMAD (FMA pipe)
 Konst runtime_konst() {
-    return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu, 0u, 256u};
+    return Konst{1u, 2u, 0xFFFFFFFFu, 0xFFFFFFFEu, 0xFFFFFF00u, 0xFF80FF80u, 0x3F3F3F3Fu, 0x7F7F7F7Fu, 0u, 256u, 0x80000000u, 1u << 26};
 }
 
 // Decode variant of a code on a device (fixed at code creation: the split variant has its own

@@ -19,7 +19,7 @@ namespace qkd {
 // to the compiler); in_regs() pins them in ordinary registers so ptxas neither folds them nor
 // re-materialises them per use.
 struct Konst {
-    uint32_t one, two, m1, m2, m256, b128, c63, c127, zero, p256;
+    uint32_t one, two, m1, m2, m256, b128, c63, c127, zero, p256, p31, p26;
     __device__ __forceinline__ Konst in_regs() const {
         Konst k;
         asm volatile("mov.b32 %0, %1;" : "=r"(k.one) : "r"(one));
@@ -32,6 +32,13 @@ struct Konst {
         asm volatile("mov.b32 %0, %1;" : "=r"(k.c127) : "r"(c127));
         k.zero = zero;   // used only as an opaque operand (scheduling dependencies), not pinned
         asm volatile("mov.b32 %0, %1;" : "=r"(k.p256) : "r"(p256));
+#if QKD_TAU_WIDE == 2
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.p31) : "r"(p31));
+        asm volatile("mov.b32 %0, %1;" : "=r"(k.p26) : "r"(p26));
+#else
+        k.p31 = p31;
+        k.p26 = p26;
+#endif
         return k;
     }
 };
@@ -107,8 +114,32 @@ __device__ __forceinline__ uint32_t tau4(uint32_t a, uint32_t b, const Konst& K)
 //   (l>=3: d<2 -> 1+1, d in 2..3 -> 1+0, d in 4..5 -> 0+1, d>=6 -> 0;  l in 1..2: [d<4];  l = 0: 0)
 // and d in {0,1,4,5} <=> (d & 0x3A) == 0 for d <= 63 (bits 1, 3, 4, 5 clear), so two masked flag
 // words replace three.  Checked against Algorithm 1 over all 64 x 64 inputs on the device (qkd_tau_table).
+#ifndef QKD_TAU_WIDE
+#define QKD_TAU_WIDE 0   // experiment (bit-exact, slower: C5a +3.9 % with 1, +13 % with 3; profiles/r2q_ab.txt)
+#endif
 __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K) {
     const uint32_t d = __vabsdiffu4(a, b);                       // ALU
+#if QKD_TAU_WIDE
+    // Right shifts on the FMA pipe as the high word of a wide multiply by an opaque power of two (IMAD.WIDE):
+    // bit 0: g = hi((a + b + d) 2^31) instead of SHF;  bit 1: c = hi(y 2^26) + a plain add instead of LEA.HI.
+    unsigned long long w1;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(w1) : "r"(a + b + d), "r"(K.p31));
+    const uint32_t g = (uint32_t)(w1 >> 32);
+    const uint32_t z = g + 0x01010101u;
+    const uint32_t p = g + 0x03030303u;
+    const uint32_t W = d + 0x3C3C3C3Cu;
+    const uint32_t Ep = (d & 0x3A3A3A3Au) + 0x3F3F3F3Fu;
+    const uint32_t t1 = lop3i<0x02, 0x40404040u>(z, W);
+    const uint32_t t2 = lop3i<0x02, 0x40404040u>(p, Ep);
+    const uint32_t y = t1 + t2;
+#if QKD_TAU_WIDE & 2
+    unsigned long long w2;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(w2) : "r"(y), "r"(K.p26));
+    return g + (uint32_t)(w2 >> 32);
+#else
+    return g + (y >> 6);
+#endif
+#else
 #if QKD_TAU_IMAD
     const uint32_t g = imad(a, K.one, imad(b, K.one, d)) >> 1;   // 2 IMAD + SHF (experiment)
 #else
@@ -141,6 +172,7 @@ __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K
     const uint32_t g2 = lop3<0xF8>(t2, p, A);                    // t2 | (p & A)
     const uint32_t y = imad(g1, K.one, g2);                      // 64 c per byte (g1 => g2: <= 0x80)
     return g + (y >> 6);                                         // LEA.HI: 63 - (l - c)
+#endif
 #endif
 }
 
