@@ -114,7 +114,11 @@ __device__ __forceinline__ EdgeIn edge_in(uint32_t e, uint32_t tw, const Konst& 
     // lanes {1,3}: e + 256 - T.  prmt(e, one) = hi16z(e) with byte 0 of K.one (0x01) in bytes 1, 3,
     // i.e. + 0x01000100, so the subtraction stays one IMAD (FMA pipe)
     r.xhi = imad(hi16z(tw), K.m1, prmt<0x4341u>(e, K.one));
+#if QKD_EIN_FMA   // experiment: the three-term sum on the FMA pipe (2 IMAD instead of 1 IADD3)
+    r.xlo = imadi<-256>(r.xhi, imad(tw, K.m1, imad(e, K.one, 0x01010100u)));
+#else
     r.xlo = imadi<-256>(r.xhi, e - tw + 0x01010100u);    // lanes {0,2}: (e + S) - 256 * xhi
+#endif
     const uint32_t clo = relu_min(r.xlo, K.b128, 0x007E007Eu);   // clamp(X - 128, 0, 126)
     const uint32_t chi = relu_min(r.xhi, K.b128, 0x007E007Eu);
     r.cw = pack16c(clo, chi, K);      // bytes in [0, 126]; bit 6 = (x >= 1) -- x = 0 counts as

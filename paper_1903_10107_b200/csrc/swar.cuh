@@ -139,6 +139,17 @@ __device__ __forceinline__ uint32_t tau4c(uint32_t a, uint32_t b, const Konst& K
 #else
     return g + (y >> 6);
 #endif
+#elif QKD_TAU_S
+    // experiment: the l-flags from s = 2g (bit 7) so the shift leaves the dependent chain; costs a second LEA.HI
+    const uint32_t s = a + b + d;
+    const uint32_t g = s >> 1;
+    const uint32_t z = s + 0x02020202u;                          // bit7: l == 0
+    const uint32_t p = s + 0x06060606u;                          // bit7: l <= 2
+    const uint32_t W = d + 0x7C7C7C7Cu;                          // bit7: d >= 4
+    const uint32_t Ep = (d & 0x3A3A3A3Au) + 0x7F7F7F7Fu;         // bit7: d not in {0,1,4,5}
+    const uint32_t t1 = lop3i<0x02, 0x80808080u>(z, W);
+    const uint32_t t2 = lop3i<0x02, 0x80808080u>(p, Ep);
+    return g + (t1 >> 7) + (t2 >> 7);
 #else
 #if QKD_TAU_IMAD
     const uint32_t g = imad(a, K.one, imad(b, K.one, d)) >> 1;   // 2 IMAD + SHF (experiment)
